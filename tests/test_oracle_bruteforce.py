@@ -1,0 +1,53 @@
+"""Pin the oracle's TC recursion to the DEFINITION of the ask and bid:
+superhedging LPs on the non-recombining path tree (tests/bruteforce.py), which
+share no code with the oracle.  N <= 3 (the bid enumerates all stopping times)."""
+import pytest
+
+import bruteforce as B
+import oracle as O
+
+MARKETS = [
+    # (S0, K, K2, T, sigma, R, kind)
+    (100.0, 100.0, 0.0, 0.25, 0.2, 0.1, O.PUT),     # the paper's Ex. 5.1 put
+    (100.0, 100.0, 0.0, 0.25, 0.2, 0.1, O.CALL),
+    (100.0, 95.0, 105.0, 0.25, 0.2, 0.1, O.BULL),    # the paper's bull spread
+    (100.0, 110.0, 0.0, 0.01, 0.1, 0.05, O.PUT),     # small h -> large k/h
+    (100.0, 90.0, 0.0, 0.01, 0.1, 0.05, O.CALL),
+    (100.0, 92.0, 108.0, 0.01, 0.15, 0.0, O.BULL),
+]
+KS = [0.0, 0.005, 0.02, 0.1]
+
+
+@pytest.mark.parametrize("N", [1, 2])
+@pytest.mark.parametrize("k", KS)
+@pytest.mark.parametrize("m", range(len(MARKETS)))
+def test_ask_bid_match_lp(m, k, N):
+    S0, K, K2, T, sigma, R, kind = MARKETS[m]
+    q = O.price_tc(O.Option(S0, K, T, sigma, R, k, kind, K2), N)
+    assert q.status == 0
+    ask = B.ask_lp(S0, K, T, sigma, R, k, N, kind, K2)
+    bid = B.bid_enum(S0, K, T, sigma, R, k, N, kind, K2)
+    scale = max(1.0, abs(ask))
+    assert abs(q.ask - ask) <= 1e-8 * scale
+    assert abs(q.bid - bid) <= 1e-8 * scale
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("k", [0.005, 0.05])
+@pytest.mark.parametrize("m", [0, 1, 2, 4])
+def test_ask_bid_match_lp_n3(m, k):
+    S0, K, K2, T, sigma, R, kind = MARKETS[m]
+    q = O.price_tc(O.Option(S0, K, T, sigma, R, k, kind, K2), 3)
+    ask = B.ask_lp(S0, K, T, sigma, R, k, 3, kind, K2)
+    bid = B.bid_enum(S0, K, T, sigma, R, k, 3, kind, K2)
+    assert abs(q.ask - ask) <= 1e-8 * max(1.0, abs(ask))
+    assert abs(q.bid - bid) <= 1e-8 * max(1.0, abs(ask))
+
+
+def test_ask_lp_n4():
+    """The ask LP alone is cheap at N = 4 (63 path nodes)."""
+    for m in (0, 1, 4):
+        S0, K, K2, T, sigma, R, kind = MARKETS[m]
+        q = O.price_tc(O.Option(S0, K, T, sigma, R, 0.01, kind, K2), 4)
+        ask = B.ask_lp(S0, K, T, sigma, R, 0.01, 4, kind, K2)
+        assert abs(q.ask - ask) <= 1e-8 * max(1.0, abs(ask))

@@ -1,0 +1,119 @@
+"""Pins of the oracle by closed forms, exact identities and invariants.
+
+  * k = 0: ask = bid = frictionless CRR American price (derived SURVEY A.1; the
+    paper states pi^a_k0 = pi^b_k0 at P:364).  Two independent code paths:
+    PWL recursion with the extra level N+1 vs scalar induction without it.
+  * European CRR induction = closed-form binomial sum (log-space weights).
+  * closed form -> Black-Scholes as N grows (textbook limit).
+  * put-call parity of the European binomial prices (exact in the model).
+  * American call without dividends = European call at k = 0.
+  * ask non-decreasing and bid non-increasing in k; bid <= CRR <= ask;
+    trivial-hedge bounds; Fig. 9 ordering chain.
+"""
+import math
+
+import numpy as np
+import pytest
+from scipy.stats import norm
+
+import oracle as O
+
+PAPER_PUT = dict(S0=100.0, K=100.0, T=0.25, sigma=0.2, R=0.1)  # P:362 / P:389
+
+
+@pytest.mark.parametrize("N", [1, 5, 20, 100, 400])
+@pytest.mark.parametrize("kind,K,K2", [(O.PUT, 100.0, 0.0), (O.CALL, 100.0, 0.0), (O.BULL, 95.0, 105.0),
+                                       (O.PUT, 85.0, 0.0), (O.CALL, 115.0, 0.0)])
+def test_k0_equals_crr(N, kind, K, K2):
+    o = O.Option(100.0, K, 0.25, 0.2, 0.1, 0.0, kind, K2)
+    q = O.price_tc(o, N)
+    crr = O.price_crr(o, N)
+    assert q.status == 0
+    assert q.ask == pytest.approx(crr, rel=1e-11, abs=1e-12)
+    assert q.bid == pytest.approx(crr, rel=1e-11, abs=1e-12)
+
+
+@pytest.mark.parametrize("N", [1, 7, 64, 500, 1500])
+@pytest.mark.parametrize("kind", [O.PUT, O.CALL, O.BULL])
+def test_european_induction_equals_closed_form(N, kind):
+    o = O.Option(100.0, 105.0 if kind != O.BULL else 95.0, 0.7, 0.35, 0.04, 0.0, kind, 115.0, american=False)
+    assert O.price_crr(o, N) == pytest.approx(O.price_euro_closed(o, N), rel=1e-11, abs=1e-13)
+
+
+def _bs(S, K, T, sigma, R, call):
+    d1 = (math.log(S / K) + (R + 0.5 * sigma ** 2) * T) / (sigma * math.sqrt(T))
+    d2 = d1 - sigma * math.sqrt(T)
+    if call:
+        return S * norm.cdf(d1) - K * math.exp(-R * T) * norm.cdf(d2)
+    return K * math.exp(-R * T) * norm.cdf(-d2) - S * norm.cdf(-d1)
+
+
+@pytest.mark.parametrize("call", [False, True])
+def test_closed_form_black_scholes_limit(call):
+    o = O.Option(100.0, 100.0, 1.0, 0.3, 0.05, 0.0, O.CALL if call else O.PUT, american=False)
+    bs = _bs(100.0, 100.0, 1.0, 0.3, 0.05, call)
+    assert abs(O.price_euro_closed(o, 4000) - bs) < 5e-3  # O(1/N) binomial error
+
+
+@pytest.mark.parametrize("N", [3, 100, 1024])
+def test_put_call_parity(N):
+    S0, K, T, sigma, R = 100.0, 93.0, 0.8, 0.25, 0.07
+    c = O.price_euro_closed(O.Option(S0, K, T, sigma, R, 0.0, O.CALL, american=False), N)
+    p = O.price_euro_closed(O.Option(S0, K, T, sigma, R, 0.0, O.PUT, american=False), N)
+    assert c - p == pytest.approx(S0 - K * math.exp(-R * T), rel=1e-11)
+
+
+@pytest.mark.parametrize("N", [10, 300, 1024])
+@pytest.mark.parametrize("R", [0.0, 0.03, 0.1])
+def test_american_call_equals_european(N, R):
+    a = O.price_crr(O.Option(100.0, 97.0, 1.3, 0.4, R, 0.0, O.CALL), N)
+    e = O.price_crr(O.Option(100.0, 97.0, 1.3, 0.4, R, 0.0, O.CALL, american=False), N)
+    assert a == pytest.approx(e, rel=1e-12)
+
+
+@pytest.mark.parametrize("kind,K,K2", [(O.PUT, 100.0, 0.0), (O.CALL, 100.0, 0.0), (O.BULL, 95.0, 105.0)])
+def test_monotone_in_k_and_ordering(kind, K, K2):
+    N = 150
+    base = O.Option(100.0, K, 0.25, 0.2, 0.1, 0.0, kind, K2)
+    crr = O.price_crr(base, N)
+    prev = None
+    for k in [0.0, 0.001, 0.0025, 0.005, 0.01, 0.02, 0.05]:
+        q = O.price_tc(O.Option(100.0, K, 0.25, 0.2, 0.1, k, kind, K2), N)
+        assert q.bid <= crr + 1e-12 <= q.ask + 2e-12
+        if prev is not None:
+            assert q.ask >= prev.ask - 1e-12
+            assert q.bid <= prev.bid + 1e-12
+        # trivial-hedge bounds
+        xi0 = {O.PUT: K - 100.0, O.CALL: 100.0 - K, O.BULL: max(100.0 - K, 0) - max(100.0 - K2, 0)}[kind]
+        assert q.bid >= max(xi0, 0.0) - 1e-12
+        assert q.ask >= max(xi0, 0.0) - 1e-12
+        bound = {O.PUT: K, O.CALL: 100.0, O.BULL: K2 - K}[kind]
+        assert q.ask <= bound + 1e-12
+        prev = q
+
+
+def test_fig9_ordering_chain():
+    """for S0 in [90, 110], pi^b_k2 <= pi^b_k1 <= pi_k0 < pi^a_k1 < pi^a_k2
+    with k0 = 0, k1 = 0.25%, k2 = 0.5% (N unstated; reading A16 -> any N, here 200)."""
+    N = 200
+    for S0 in range(90, 111, 2):
+        p = lambda k: O.price_tc(O.Option(float(S0), 100.0, 0.25, 0.2, 0.1, k, O.PUT), N)
+        q0, q1, q2 = p(0.0), p(0.0025), p(0.005)
+        assert q0.ask == pytest.approx(q0.bid, rel=1e-11)
+        assert q2.bid <= q1.bid + 1e-12 <= q0.bid + 2e-12
+        assert q0.ask < q1.ask < q2.ask
+
+
+def test_invalid_inputs():
+    bad = [
+        O.Option(-1.0, 100.0, 1.0, 0.2, 0.05, 0.0),
+        O.Option(100.0, 100.0, 0.0, 0.2, 0.05, 0.0),
+        O.Option(100.0, 100.0, 1.0, 0.0, 0.05, 0.0),
+        O.Option(100.0, 100.0, 1.0, 0.2, 0.05, 1.0),
+        O.Option(100.0, 100.0, 1.0, 0.2, 0.05, -0.1),
+        O.Option(100.0, 105.0, 1.0, 0.2, 0.05, 0.0, O.BULL, 95.0),
+    ]
+    for o in bad:
+        assert O.price_tc(o, 10).status == O.EINVAL
+    # arbitrage: r >= u  (R T/N >= sigma sqrt(T/N))
+    assert O.price_tc(O.Option(100.0, 100.0, 1.0, 0.01, 0.5, 0.0), 4).status == O.EARBITRAGE
