@@ -120,9 +120,13 @@ static double pwl_eval(const pwl *p, double y)
     int n = p->n;
     if (y <= p->x[0]) return p->f[0] + p->sl * (y - p->x[0]);
     if (y >= p->x[n - 1]) return p->f[n - 1] + p->sr * (y - p->x[n - 1]);
-    /* find piece [x_i, x_{i+1}] containing y (linear scan: plain) */
-    int i = 0;
-    while (!(y <= p->x[i + 1])) i++;
+    /* find the piece [x_i, x_{i+1}] containing y by bisection */
+    int i = 0, hi = n - 1; /* invariant: x[i] < y <= x[hi] */
+    while (hi - i > 1) {
+        int mid = (i + hi) / 2;
+        if (p->x[mid] < y) i = mid;
+        else hi = mid;
+    }
     double t = (y - p->x[i]) / (p->x[i + 1] - p->x[i]);
     return p->f[i] + t * (p->f[i + 1] - p->f[i]);
 }
@@ -130,11 +134,11 @@ static double pwl_eval(const pwl *p, double y)
 /*
  * Canonical form (reading R10, SPEC "canonicalize"): drop every vertex that is
  * not a kink.  "Not a kink" is decided on VALUES, not on difference-quotient
- * slopes (which are noisy on short pieces): a run of vertices is dropped when
- * every vertex of the run lies within CANON_ATOL * max(1, max|f|) of the chord
- * that replaces it -- the segment between the kept neighbours, or, at either
- * end, the tail line (whose slope is kept) through the kept neighbour.
- * Dropping therefore changes the function by at most that amount everywhere.
+ * slopes (which are noisy on short pieces): vertex i is dropped when it, and
+ * the first vertex of the run of dropped vertices before it, lie within
+ * CANON_ATOL * max(1, max|f|) of the chord that replaces them -- the segment
+ * from the last kept vertex to vertex i+1, or, at either end, the tail line
+ * (whose slope is kept) through the kept neighbour.
  * The function keeps at least one vertex (a line is one anchor vertex).
  */
 #define CANON_ATOL 1e-14
@@ -167,8 +171,11 @@ static void pwl_canonicalize(pwl *p)
                and a line keeps its anchor anyway */
             droppable = 0;
         } else {
-            for (int q = prev + 1; q <= i && droppable; q++)
-                if (fabs(p->f[q] - chord_at(p, prev, next, p->x[q])) > tol) droppable = 0;
+            /* vertex i and the first vertex of the current run of dropped
+               vertices must both lie on the replacing chord (O(1) per vertex) */
+            if (fabs(p->f[i] - chord_at(p, prev, next, p->x[i])) > tol) droppable = 0;
+            if (prev + 1 < i && fabs(p->f[prev + 1] - chord_at(p, prev, next, p->x[prev + 1])) > tol)
+                droppable = 0;
         }
         keep[i] = !droppable;
         if (keep[i]) prev = i;
@@ -226,7 +233,7 @@ static int pwl_envelope(const pwl *f, const pwl *g, int want_max, pwl *out, coun
     }
     if (pwl_init(out, 2 * nc + 2) != OR_OK) { free(X); return OR_ENOMEM; }
 
-    double *D = (double *)malloc(sizeof(double) * (size_t)nc);
+    double *D = (double *)calloc((size_t)nc, sizeof(double));
     double *F = (double *)malloc(sizeof(double) * (size_t)nc);
     double *G = (double *)malloc(sizeof(double) * (size_t)nc);
     for (int i = 0; i < nc; i++) {
