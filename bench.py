@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""Benchmark of the amtc hot path (BASELINE.json metric) -- one JSON line.
+
+Default workload (BASELINE.json config 4): 16384 American options per GPU
+(45% put, 45% call, 10% bull spread; seeded synthetic), N = 1500 steps, ask AND
+bid under proportional costs k ~ U[0, 2%], fp64.  One "step" = pricing the
+whole batch through the C-ABI (amtc_price_american_tc_batch, inputs resident in
+HBM).  Multi-GPU: one process per GPU (torchrun); each rank prices its own
+16384-option batch (seed + rank) with no data-path collective -> weak scaling;
+timing = max over ranks of the device time (CUDA events), whole-job value =
+all ranks' node-updates / that time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4|2] [--impl amtc|reference]
+
+--impl reference times the CPU oracle (oracle/, plain C) on a bounded sample of
+the same workload on this host's cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASELINE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
+METRIC = BASELINE["metric"]
+
+# FP64 roofline: 148 SMs x 64 FP64 lanes/clk x 2 flop/FMA x clock (B200_PROFILING.md
+# unit counts; MEASURED_PEAKS.json has no FP64 figure).  See DESIGN.md "Roofline".
+FP64_LANES_PER_SM = 64
+# algorithmic FP64 cost model: 12 flop per child vertex per node-update
+TC_FLOP_PER_CHILD_VERTEX = 12.0
+CRR_FLOP_PER_NODE = 6.0  # DFMA(X) + DMUL + DFMA + DMNMX = 2 + 1 + 2 + 1
+
+
+def tc_nodes(N: int) -> int:
+    """node-updates per option at levels 0..N: (N+1)(N+2)/2."""
+    return (N + 1) * (N + 2) // 2
+
+
+def crr_nodes(N: int) -> int:
+    return N * (N + 1) // 2
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clock and throttle reasons during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def flush_l2(buf):
+    buf.add_(1.0)  # 512 MiB read+write > 126 MB L2
+
+
+def setup_dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if __import__("torch").cuda.is_available() else "gloo")
+        pg = dist
+    return world, rank, local, pg
+
+
+def max_over_ranks(x: float, pg, device) -> float:
+    if pg is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, pg, device) -> float:
+    if pg is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    pg.all_reduce(t, op=pg.ReduceOp.SUM)
+    return float(t.item())
+
+
+def workload(config: int, rank: int):
+    from paper_1110_2477_b200 import workloads as W
+    if config == 4:
+        b = W.config4(seed=W.SEED_BASE + 4 + 1000 * rank)
+        return b, W.CONFIG4_N, "config4: American put/call/bull-spread batch, ask+bid under proportional costs"
+    if config == 2:
+        b = W.config2(seed=W.SEED_BASE + 2 + 1000 * rank)
+        return b, W.CONFIG2_N, "config2: zero-cost American put/call batch (CRR), one tree per warp"
+    raise SystemExit(f"unknown --config {config}")
+
+
+def cpu_baseline(config: int, budget_options: int = 8, seed: int = 123) -> dict:
+    """The oracle as it stands, on all host cores, on a bounded seeded sample."""
+    import oracle as O
+    from paper_1110_2477_b200 import workloads as W
+    b, N, _ = workload(config, 0)
+    idx = np.sort(np.random.default_rng(seed).choice(len(b), budget_options, replace=False))
+    cores = len(os.sched_getaffinity(0))
+    opts = []
+    for i in idx:
+        r = b.row(int(i))
+        opts.append(O.Option(r["S0"], r["K"], r["T"], r["sigma"], r["R"], r["k"], r["kind"], r["K2"]))
+    t0 = time.perf_counter()
+    if config == 4:
+        O.price_tc_many(opts, N, threads=cores)
+        nodes = tc_nodes(N) * len(opts)
+    else:
+        O.price_crr_many(opts, N, threads=cores)
+        nodes = crr_nodes(N) * len(opts)
+    dt = time.perf_counter() - t0
+    return {"value": nodes / dt, "unit": "node-updates/s", "cores": min(cores, len(opts)), "kind": "oracle",
+            "sample": f"{len(opts)} options of the config-{config} batch (numpy default_rng({seed}) choice), "
+                      f"N={N}, one option per thread, {dt:.1f} s wall",
+            "options_per_s": len(opts) / dt}
+
+
+def run_reference(args):
+    world, rank, local, pg = setup_dist()
+    if rank != 0:
+        return 0
+    times = []
+    res = None
+    for i in range(args.warmup + args.steps):
+        res = cpu_baseline(args.config, budget_options=args.ref_options, seed=123 + i)
+        if i >= args.warmup:
+            times.append(res)
+    vals = [r["value"] for r in times]
+    value = float(np.mean(vals))
+    b, N, desc = workload(args.config, 0)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "node-updates/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": float(np.mean([args.ref_options * tc_nodes(N) / r["value"] * 1e3 for r in times])),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": desc, "N": N, "options_per_step": args.ref_options},
+            "cpu_baseline": {"value": value, "unit": "node-updates/s", "cores": times[-1]["cores"],
+                             "kind": "oracle", "sample": times[-1]["sample"]},
+            "e2e": {"value": value, "unit": "node-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_amtc(args):
+    import torch
+    world, rank, local, pg = setup_dist()
+    assert torch.cuda.is_available(), "bench.py needs a CUDA device"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_1110_2477_b200 import api, build
+    build.build()
+    api.lib()
+    b, N, desc = workload(args.config, rank)
+    n = len(b)
+    cols = api.device_batch(b, dev)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device=dev)
+    if args.config == 4:
+        out = torch.empty(n * 24, dtype=torch.uint8, device=dev)
+        step = lambda: api.price_american_tc_batch(cols, N, out, stream)
+        nodes_per_step = tc_nodes(N) * n
+    else:
+        out = torch.empty(n, dtype=torch.float64, device=dev)
+        step = lambda: api.price_crr_batch(cols, N, out, stream)
+        nodes_per_step = crr_nodes(N) * n
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
+    if pg is not None:
+        pg.barrier()
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.start()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = api.launch_count()
+    kernel_ms, vertex_sum = 0.0, 0
+    for i in range(args.steps):
+        flush_l2(flush)
+        starts[i].record(stream)
+        step()
+        ends[i].record(stream)
+        if args.config == 4:
+            st = api.tc_last_stats()
+            kernel_ms += st["solve_ms"]
+            vertex_sum += st["vertex_sum"]
+    torch.cuda.synchronize()
+    launches = api.launch_count() - launches0
+    if pg is not None:
+        pg.barrier()
+    torch.cuda.synchronize()
+    clocks = sampler.stop() if sampler else None
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = max_over_ranks(float(np.sum(step_ms)), pg, dev)
+    total_nodes = sum_over_ranks(float(nodes_per_step * args.steps), pg, dev)
+    total_opts = sum_over_ranks(float(n * args.steps), pg, dev)
+    value = total_nodes / (total_ms / 1e3)
+
+    # roofline of the dominant kernel
+    props = torch.cuda.get_device_properties(dev)
+    sm_count = props.multi_processor_count
+    clk = (clocks or {}).get("sm_max_mhz") or 1965.0
+    peak_tflops = sm_count * FP64_LANES_PER_SM * 2 * clk * 1e6 / 1e12
+    if args.config == 4:
+        kern_ms = kernel_ms / args.steps
+        flop = TC_FLOP_PER_CHILD_VERTEX * 2.0 * vertex_sum / args.steps
+        kname = "tc_solve_kernel"
+    else:
+        # the CRR step is a single kernel launch: its event time is the step time
+        kern_ms = float(np.mean(step_ms))
+        flop = CRR_FLOP_PER_NODE * nodes_per_step
+        kname = "crr_kernel"
+    achieved = flop / (kern_ms / 1e3) / 1e12
+    roofline = {"bound": "alu", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
+                "frac": achieved / peak_tflops, "traffic": None, "kernel": kname,
+                "kernel_ms_per_step": kern_ms,
+                "peak_source": f"derived: {sm_count} SMs x 64 FP64/clk x 2 x {clk:.0f} MHz "
+                               "(no FP64 entry in MEASURED_PEAKS.json)",
+                "flop_model": ("12 flop per child vertex per node-update (DESIGN.md)" if args.config == 4
+                               else "6 flop per CRR node-update (DESIGN.md)")}
+    if args.config == 4:
+        roofline["vertex_sum_per_step"] = vertex_sum / args.steps
+
+    # end to end through the public C-ABI with HOST buffers (pinned), H2D + D2H inside
+    e2e = None
+    if not args.no_e2e:
+        pinned = {f: torch.from_numpy(np.ascontiguousarray(getattr(b, f))).pin_memory()
+                  for f in ("S0", "K", "K2", "T", "sigma", "R", "k", "kind")}
+        hb = {f: t.numpy() for f, t in pinned.items()}
+        h2d = sum(t.numel() * t.element_size() for t in pinned.values())
+        e2e_steps = max(1, min(args.steps, 3))
+        if pg is not None:
+            pg.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            if args.config == 4:
+                q, rc = api.price_american_tc_batch_host(hb, N, stream)
+                d2h = q.nbytes
+            else:
+                q = api.price_crr_batch_host(hb, N, stream)
+                d2h = q.nbytes
+        torch.cuda.synchronize()
+        e2e_s = max_over_ranks(time.perf_counter() - t0, pg, dev)
+        e2e = {"value": sum_over_ranks(float(nodes_per_step * e2e_steps), pg, dev) / e2e_s,
+               "unit": "node-updates/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "steps": e2e_steps, "timer": "host wall clock around the synchronous C-ABI call"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config, budget_options=args.ref_options)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "node-updates/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": desc, "N": N, "options_per_gpu": n, "options_total": int(total_opts / args.steps),
+                           "options_per_s": total_opts / (total_ms / 1e3),
+                           "node_updates_per_option": tc_nodes(N) if args.config == 4 else crr_nodes(N),
+                           "l2": "flushed before every timed step (512 MiB write, untimed)",
+                           "parallelism": f"dp{world} (independent options per rank, no collective)"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clocks, "step_ms": step_ms}
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.barrier()
+        pg.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4, choices=[2, 4])
+    ap.add_argument("--impl", default="amtc", choices=["amtc", "reference"])
+    ap.add_argument("--ref-options", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_amtc(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,148 @@
+/*
+ * amtc.h -- C-ABI of the B200-native American-option ask/bid pricer under
+ * proportional transaction costs (Zhang, Roux & Zastawniak 2011).
+ *
+ * Citations: P:n = PAPER.md line n.
+ *
+ * All arithmetic is IEEE fp64 on the GPU (sm_100a).  Every pointer is owned by
+ * the caller; the library keeps only lazily created per-device scratch
+ * workspaces (guarded by a mutex) that it reuses across calls.  No C++
+ * exception crosses this boundary.  Functions return an amtc_status (0 = OK);
+ * per-option failures leave NaN prices and a non-zero per-option status.
+ *
+ * Model (Sec. 4.1): N steps, u = exp(sigma sqrt(T/N)), d = 1/u,
+ * r = exp(R T / N); stock price S0 u^(t-j) d^j at node (t, j) (j = number of
+ * down-moves); stock ask/bid (1+k)S, (1-k)S for t >= 1 and S0 at t = 0
+ * (P:92); an extra time instant t = N+1 with payoff (0,0).
+ */
+#ifndef AMTC_H
+#define AMTC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* payoff kinds (the payoff process (xi, zeta) of P:94) */
+typedef enum {
+    AMTC_PUT = 0,        /* physical delivery: (xi, zeta) = (K, -1)  */
+    AMTC_CALL = 1,       /* physical delivery: (-K, +1)            (reading R6)       */
+    AMTC_BULL_SPREAD = 2 /* cash: ((S-K)^+ - (S-K2)^+, 0), K < K2 */
+} amtc_kind;
+
+/* status codes (per option and per call; a call returns the worst status) */
+typedef enum {
+    AMTC_OK = 0,
+    AMTC_EINVAL = 1,      /* S0, K, T, sigma <= 0; N < 1; k not in [0,1); bull with K >= K2;
+                             unknown kind; null pointer                                     */
+    AMTC_EARBITRAGE = 2,  /* not d < r < u (risk-neutral p outside (0,1))                   */
+    AMTC_ECAPACITY = 3,   /* a node function outgrew every scratch capacity tried           */
+    AMTC_EUNBOUNDED = 4,  /* slope restriction infimum is -inf (impossible when d<r<u)      */
+    AMTC_ECUDA = 5,       /* a CUDA runtime error (message: amtc_last_error())              */
+    AMTC_ENCCL = 6
+} amtc_status;
+
+/* market and tenor of one option */
+typedef struct {
+    double S0;    /* spot price at t = 0, > 0                       */
+    double T;     /* expiry in years, > 0                           */
+    double sigma; /* volatility, > 0                                */
+    double R;     /* continuously compounded annual interest rate   */
+} amtc_params;
+
+/* payoff of one option */
+typedef struct {
+    int32_t kind;   /* amtc_kind                                   */
+    uint32_t flags; /* reserved, must be 0                         */
+    double K;       /* strike (bull spread: the long strike K1)    */
+    double K2;      /* bull spread: the short strike, > K; else 0  */
+} amtc_payoff;
+
+/* result for one option (24 bytes) */
+typedef struct {
+    double ask;      /* pi^a_0 = z_0(0) of the seller recursion  */
+    double bid;      /* pi^b_0 = -z'_0(0) of the buyer recursion */
+    int32_t status;  /* amtc_status of this option                               */
+    int32_t max_bp;  /* largest vertex count of any node function (capacity audit) */
+} amtc_quote;
+
+/* Structure-of-arrays batch of n options.  For the *_batch calls every
+   pointer is a DEVICE pointer (fp64 / int32 arrays of length n); for the
+   *_batch_host calls every pointer is a HOST pointer. */
+typedef struct {
+    const double* S0;
+    const double* K;
+    const double* K2;     /* may be NULL when no option is a bull spread */
+    const double* T;
+    const double* sigma;
+    const double* R;
+    const double* k;      /* proportional transaction cost rate, in [0,1); may be NULL for CRR */
+    const int32_t* kind;  /* amtc_kind */
+} amtc_batch_soa;
+
+/*
+ * North-star call: ask and bid of ONE American option under proportional
+ * costs k on an N-step tree (Sec. 3 seller/buyer recursions).
+ * Synchronous; runs on the current CUDA device.  On error the quote carries
+ * NaN prices and the status.
+ */
+amtc_quote amtc_price_american_tc(const amtc_params* params, int32_t N, const amtc_payoff* payoff,
+                                  double k);
+
+/*
+ * Batched ask/bid for n independent options on N-step trees (DEVICE pointers).
+ * d_out: device array of n amtc_quote.  Work is enqueued on cuda_stream
+ * (a cudaStream_t, NULL = legacy default stream); the call synchronises that
+ * stream once at the end (to re-run any option whose node functions outgrew
+ * the first scratch capacity), so d_out is complete on return.
+ * Returns the worst per-option status, or AMTC_ECUDA.
+ */
+int amtc_price_american_tc_batch(const amtc_batch_soa* d_in, int64_t n, int32_t N, amtc_quote* d_out,
+                                 void* cuda_stream);
+
+/* As above with HOST pointers: copies inputs host->device and quotes
+   device->host inside the call (h_out: host array of n amtc_quote). */
+int amtc_price_american_tc_batch_host(const amtc_batch_soa* h_in, int64_t n, int32_t N,
+                                      amtc_quote* h_out, void* cuda_stream);
+
+/*
+ * k = 0 (frictionless) batched CRR American prices (Appendix: no
+ * extra level, scalar max(exercise, continuation)).  d_in->k and ->K2 are
+ * ignored except for bull spreads (K2).  d_price: device array of n doubles.
+ * Asynchronous on cuda_stream.  Per-option validation failures write NaN.
+ */
+int amtc_price_crr_batch(const amtc_batch_soa* d_in, int64_t n, int32_t N, double* d_price,
+                         void* cuda_stream);
+
+/* As above with HOST pointers (synchronous). */
+int amtc_price_crr_batch_host(const amtc_batch_soa* h_in, int64_t n, int32_t N, double* h_price,
+                              void* cuda_stream);
+
+/* Human-readable name of a status code (static storage). */
+const char* amtc_strerror(int status);
+
+/* Message of the last CUDA error seen by this thread (static storage per thread). */
+const char* amtc_last_error(void);
+
+/* Number of kernels this library has launched in this process (monotonic). */
+int64_t amtc_launch_count(void);
+
+/* Work statistics of the last amtc_price_american_tc_batch* call on the
+   current device (for throughput / roofline accounting). */
+typedef struct {
+    int64_t vertex_sum;    /* sum over all node-updates t = N..1, both parties, of the
+                              vertex count of the produced node function z_t(j)     */
+    int32_t passes;        /* solver passes run (1 + capacity retries)               */
+    int32_t pad;
+    int64_t retried_items; /* (option, party) items re-run with larger scratch       */
+    double solve_ms;       /* device time of the solver kernel launches (CUDA events
+                              recorded around them on the call's stream)            */
+} amtc_tc_stats;
+int amtc_tc_last_stats(amtc_tc_stats* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AMTC_H */

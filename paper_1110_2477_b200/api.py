@@ -1,0 +1,207 @@
+"""Thin ctypes binding of include/amtc.h (argument marshalling only).
+
+Every computation happens inside libamtc.so (CUDA, sm_100a, fp64).  PyTorch is
+used only for device memory and streams.  There is no CPU fallback: loading
+fails loudly when the library is missing.
+
+Names follow the C-ABI: ``price_american_tc``, ``price_american_tc_batch``,
+``price_american_tc_batch_host``, ``price_crr_batch``, ``price_crr_batch_host``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libamtc.so")
+
+PUT, CALL, BULL = 0, 1, 2
+STATUS = {0: "OK", 1: "EINVAL", 2: "EARBITRAGE", 3: "ECAPACITY", 4: "EUNBOUNDED", 5: "ECUDA", 6: "ENCCL"}
+
+
+class Params(C.Structure):
+    _fields_ = [("S0", C.c_double), ("T", C.c_double), ("sigma", C.c_double), ("R", C.c_double)]
+
+
+class Payoff(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("flags", C.c_uint32), ("K", C.c_double), ("K2", C.c_double)]
+
+
+class Quote(C.Structure):
+    _fields_ = [("ask", C.c_double), ("bid", C.c_double), ("status", C.c_int32), ("max_bp", C.c_int32)]
+
+
+class BatchSoA(C.Structure):
+    _fields_ = [("S0", C.c_void_p), ("K", C.c_void_p), ("K2", C.c_void_p), ("T", C.c_void_p),
+                ("sigma", C.c_void_p), ("R", C.c_void_p), ("k", C.c_void_p), ("kind", C.c_void_p)]
+
+
+class TcStats(C.Structure):
+    _fields_ = [("vertex_sum", C.c_int64), ("passes", C.c_int32), ("pad", C.c_int32),
+                ("retried_items", C.c_int64), ("solve_ms", C.c_double)]
+
+
+QUOTE_DTYPE = np.dtype([("ask", "<f8"), ("bid", "<f8"), ("status", "<i4"), ("max_bp", "<i4")])
+assert QUOTE_DTYPE.itemsize == C.sizeof(Quote) == 24
+
+EXPORTS = ["amtc_price_american_tc", "amtc_price_american_tc_batch", "amtc_price_american_tc_batch_host",
+           "amtc_price_crr_batch", "amtc_price_crr_batch_host", "amtc_strerror", "amtc_last_error",
+           "amtc_launch_count", "amtc_tc_last_stats"]
+
+_lib = None
+
+
+def lib():
+    """Load libamtc.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        L.amtc_price_american_tc.restype = Quote
+        L.amtc_price_american_tc.argtypes = [C.POINTER(Params), C.c_int32, C.POINTER(Payoff), C.c_double]
+        for name in ("amtc_price_american_tc_batch", "amtc_price_american_tc_batch_host"):
+            f = getattr(L, name)
+            f.restype = C.c_int
+            f.argtypes = [C.POINTER(BatchSoA), C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]
+        for name in ("amtc_price_crr_batch", "amtc_price_crr_batch_host"):
+            f = getattr(L, name)
+            f.restype = C.c_int
+            f.argtypes = [C.POINTER(BatchSoA), C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]
+        L.amtc_strerror.restype = C.c_char_p
+        L.amtc_strerror.argtypes = [C.c_int]
+        L.amtc_last_error.restype = C.c_char_p
+        L.amtc_launch_count.restype = C.c_int64
+        L.amtc_tc_last_stats.restype = C.c_int
+        L.amtc_tc_last_stats.argtypes = [C.POINTER(TcStats)]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, allow_option_status: bool = True) -> int:
+    if rc in (5, 6) or (rc != 0 and not allow_option_status):
+        msg = lib().amtc_last_error().decode()
+        raise RuntimeError(f"amtc error {STATUS.get(rc, rc)}: {msg}")
+    return rc
+
+
+def strerror(status: int) -> str:
+    return lib().amtc_strerror(status).decode()
+
+
+def launch_count() -> int:
+    return int(lib().amtc_launch_count())
+
+
+def tc_last_stats() -> dict:
+    s = TcStats()
+    lib().amtc_tc_last_stats(C.byref(s))
+    return {"vertex_sum": s.vertex_sum, "passes": s.passes, "retried_items": s.retried_items,
+            "solve_ms": s.solve_ms}
+
+
+# ---------------------------------------------------------------------------
+# single option (north star)
+# ---------------------------------------------------------------------------
+
+def price_american_tc(S0: float, K: float, T: float, sigma: float, R: float, N: int, k: float,
+                      kind: int = PUT, K2: float = 0.0) -> dict:
+    """Ask and bid of one American option under proportional costs k."""
+    p = Params(S0, T, sigma, R)
+    y = Payoff(kind, 0, K, K2)
+    q = lib().amtc_price_american_tc(C.byref(p), N, C.byref(y), k)
+    return {"ask": q.ask, "bid": q.bid, "status": q.status, "max_bp": q.max_bp}
+
+
+# ---------------------------------------------------------------------------
+# batches
+# ---------------------------------------------------------------------------
+
+_FIELDS = ("S0", "K", "K2", "T", "sigma", "R", "k", "kind")
+
+
+def _soa_from_torch(cols: dict) -> BatchSoA:
+    ptr = {f: (cols[f].data_ptr() if cols.get(f) is not None else None) for f in _FIELDS}
+    return BatchSoA(**ptr)
+
+
+def _soa_from_numpy(cols: dict):
+    keep = {}
+    for f in _FIELDS:
+        a = cols.get(f)
+        if a is None:
+            keep[f] = None
+            continue
+        dt = np.int32 if f == "kind" else np.float64
+        keep[f] = np.ascontiguousarray(a, dtype=dt)
+    soa = BatchSoA(**{f: (keep[f].ctypes.data if keep[f] is not None else None) for f in _FIELDS})
+    return soa, keep
+
+
+def device_batch(batch, device="cuda"):
+    """Copy a workloads.Batch (numpy SoA) to device tensors (dict)."""
+    import torch
+    out = {}
+    for f in _FIELDS:
+        a = getattr(batch, f)
+        out[f] = torch.from_numpy(np.ascontiguousarray(a)).to(device)
+    return out
+
+
+def _stream_handle(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def price_american_tc_batch(cols: dict, N: int, out=None, stream=None):
+    """Device batch: cols = dict of CUDA tensors (float64 / int32 'kind').
+    Returns (quotes uint8 tensor viewable as QUOTE_DTYPE, status)."""
+    import torch
+    n = int(cols["S0"].numel())
+    if out is None:
+        out = torch.empty(n * 24, dtype=torch.uint8, device=cols["S0"].device)
+    soa = _soa_from_torch(cols)
+    rc = lib().amtc_price_american_tc_batch(C.byref(soa), n, N, C.c_void_p(out.data_ptr()),
+                                            _stream_handle(stream))
+    return out, _check(rc)
+
+
+def quotes_to_numpy(out) -> np.ndarray:
+    return out.cpu().numpy().view(QUOTE_DTYPE)
+
+
+def price_american_tc_batch_host(batch, N: int, stream=None) -> tuple[np.ndarray, int]:
+    """Host batch (numpy SoA, e.g. workloads.Batch); H2D/D2H inside the call."""
+    cols = {f: getattr(batch, f) for f in _FIELDS} if not isinstance(batch, dict) else batch
+    soa, keep = _soa_from_numpy(cols)
+    n = len(keep["S0"])
+    out = np.zeros(n, dtype=QUOTE_DTYPE)
+    rc = lib().amtc_price_american_tc_batch_host(C.byref(soa), n, N, C.c_void_p(out.ctypes.data),
+                                                 _stream_handle(stream))
+    return out, _check(rc)
+
+
+def price_crr_batch(cols: dict, N: int, out=None, stream=None):
+    import torch
+    n = int(cols["S0"].numel())
+    if out is None:
+        out = torch.empty(n, dtype=torch.float64, device=cols["S0"].device)
+    soa = _soa_from_torch(cols)
+    rc = lib().amtc_price_crr_batch(C.byref(soa), n, N, C.c_void_p(out.data_ptr()), _stream_handle(stream))
+    _check(rc, allow_option_status=False)
+    return out
+
+
+def price_crr_batch_host(batch, N: int, stream=None) -> np.ndarray:
+    cols = {f: getattr(batch, f) for f in _FIELDS} if not isinstance(batch, dict) else batch
+    soa, keep = _soa_from_numpy(cols)
+    n = len(keep["S0"])
+    out = np.zeros(n, dtype=np.float64)
+    rc = lib().amtc_price_crr_batch_host(C.byref(soa), n, N, C.c_void_p(out.ctypes.data),
+                                         _stream_handle(stream))
+    _check(rc, allow_option_status=False)
+    return out

@@ -1,0 +1,357 @@
+// amtc_capi.cu -- the C-ABI of include/amtc.h (host side).
+//
+// Owns per-device scratch (grow-only, mutex-guarded), validates arguments,
+// schedules the transaction-cost passes (first pass with small per-node
+// scratch bounds for every item, then re-runs of overflowed items with larger
+// bounds and fewer resident CTAs), and marshals host buffers for the *_host
+// variants.  No exception crosses the boundary.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "amtc.h"
+#include "amtc_internal.cuh"
+#include "pwl_device.cuh"
+
+namespace amtc {
+
+static std::atomic<int64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static thread_local std::string g_last_error;
+
+static int cuda_fail(cudaError_t e, const char* what) {
+    g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+    return STATUS_ECUDA;
+}
+
+#define AMTC_CUDA(call)                                  \
+    do {                                                 \
+        cudaError_t e_ = (call);                         \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+// grow-only device buffer
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t want) {
+        if (want <= bytes) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) bytes = want;
+        return e;
+    }
+};
+
+struct DevState {
+    std::mutex mu;
+    DevBuf items[2], cls, small, ws, stage_in, stage_out;
+    int sm_count = 0;
+    int occupancy = 0;
+    // stats of the last TC batch
+    unsigned long long vertex_sum = 0;
+    int passes = 0;
+    int64_t retried = 0;
+    double solve_ms = 0.0;   // device time of the solver launches (CUDA events)
+    cudaEvent_t ev[2 * 8] = {};
+};
+
+static DevState* state_for_device(int dev) {
+    static std::mutex mu;
+    static std::vector<DevState*> states;
+    std::lock_guard<std::mutex> g(mu);
+    if ((int)states.size() <= dev) states.resize(dev + 1, nullptr);
+    if (!states[dev]) states[dev] = new DevState();
+    return states[dev];
+}
+
+static BatchPtrs to_ptrs(const amtc_batch_soa* b) {
+    BatchPtrs p;
+    p.S0 = b->S0; p.K = b->K; p.K2 = b->K2; p.T = b->T;
+    p.sigma = b->sigma; p.R = b->R; p.k = b->k; p.kind = b->kind;
+    return p;
+}
+
+static bool soa_ok(const amtc_batch_soa* b) {
+    return b && b->S0 && b->K && b->T && b->sigma && b->R && b->kind;
+}
+
+// small device scratch layout (ints)
+enum { SM_HIST = 0, SM_WORK = TC_CLASSES + 1, SM_OVF0, SM_OVF1, SM_WORST, SM_VSUM = 32, SM_INTS = 64 };
+
+struct Pass {
+    int bmul, badd, cap_per_node;
+};
+static const Pass kPasses[] = {{2, 8, 48}, {3, 16, 384}, {4, 32, 4096}, {8, 64, 32768}};
+
+static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amtc_quote* d_out,
+                           cudaStream_t s) {
+    if (!soa_ok(d_in) || !d_out || n < 0 || N < 1) return STATUS_EINVAL;
+    if (n == 0) return STATUS_OK;
+    if (2 * n > (int64_t)INT32_MAX / 2) return STATUS_EINVAL;
+    int dev = 0;
+    AMTC_CUDA(cudaGetDevice(&dev));
+    DevState* st = state_for_device(dev);
+    std::lock_guard<std::mutex> guard(st->mu);
+    if (!st->sm_count) {
+        AMTC_CUDA(cudaDeviceGetAttribute(&st->sm_count, cudaDevAttrMultiProcessorCount, dev));
+        st->occupancy = tc_solve_occupancy();
+    }
+    const int64_t n2 = 2 * n;
+    AMTC_CUDA(st->items[0].ensure(sizeof(int) * n2));
+    AMTC_CUDA(st->items[1].ensure(sizeof(int) * n2));
+    AMTC_CUDA(st->cls.ensure(n2));
+    AMTC_CUDA(st->small.ensure(sizeof(int) * SM_INTS));
+    int* small = static_cast<int*>(st->small.p);
+    Quote* out = reinterpret_cast<Quote*>(d_out);
+    BatchPtrs in = to_ptrs(d_in);
+
+    tc_launch_prepare(in, n, N, out, static_cast<unsigned char*>(st->cls.p), small + SM_HIST,
+                      static_cast<int*>(st->items[0].p), s);
+    AMTC_CUDA(cudaGetLastError());
+    AMTC_CUDA(cudaMemsetAsync(small + SM_VSUM, 0, sizeof(unsigned long long), s));
+
+    size_t free_b = 0, total_b = 0;
+    AMTC_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const size_t budget = std::min<size_t>((size_t)(0.6 * (double)(free_b + st->ws.bytes)), (size_t)48 << 30);
+
+    const int* q_items = static_cast<int*>(st->items[0].p);
+    const int* q_count = small + SM_HIST + TC_CLASSES;  // total valid items
+    int64_t queued = n2;                                // upper bound for grid sizing
+    int ovf_host = 0;
+    int passes = 0;
+    const int n_passes = (int)(sizeof(kPasses) / sizeof(kPasses[0]));
+    for (int p = 0; p < n_passes; ++p) {
+        const Pass& P = kPasses[p];
+        const int64_t cap64 = (int64_t)(N + 2) * P.cap_per_node;
+        const int arena_cap = (int)std::min<int64_t>(cap64, (int64_t)1 << 30);
+        const size_t wsb = (tc_workspace_bytes(N, arena_cap) + 255) & ~(size_t)255;
+        int64_t grid = (int64_t)st->sm_count * st->occupancy;
+        grid = std::min<int64_t>(grid, queued);
+        grid = std::min<int64_t>(grid, (int64_t)(budget / wsb));
+        if (grid < 1) break;
+        AMTC_CUDA(st->ws.ensure(wsb * (size_t)grid));
+        int* ovf_count = small + (p % 2 == 0 ? SM_OVF0 : SM_OVF1);
+        int* ovf_items = static_cast<int*>(st->items[(p + 1) % 2].p);
+        AMTC_CUDA(cudaMemsetAsync(small + SM_WORK, 0, sizeof(int), s));
+        AMTC_CUDA(cudaMemsetAsync(ovf_count, 0, sizeof(int), s));
+        if (!st->ev[0]) {
+            for (auto& e : st->ev) AMTC_CUDA(cudaEventCreate(&e));
+        }
+        TcLaunch L;
+        L.in = in;
+        L.N = N;
+        L.out = out;
+        L.items = q_items;
+        L.n_items = q_count;
+        L.work_counter = small + SM_WORK;
+        L.ovf_items = ovf_items;
+        L.ovf_count = ovf_count;
+        L.vertex_sum = reinterpret_cast<unsigned long long*>(small + SM_VSUM);
+        L.ws = static_cast<char*>(st->ws.p);
+        L.ws_stride = wsb;
+        L.arena_cap = arena_cap;
+        L.bmul = P.bmul;
+        L.badd = P.badd;
+        AMTC_CUDA(cudaEventRecord(st->ev[2 * p], s));
+        tc_launch_solve(L, (int)grid, s);
+        AMTC_CUDA(cudaGetLastError());
+        AMTC_CUDA(cudaEventRecord(st->ev[2 * p + 1], s));
+        passes++;
+        AMTC_CUDA(cudaMemcpyAsync(&ovf_host, ovf_count, sizeof(int), cudaMemcpyDeviceToHost, s));
+        AMTC_CUDA(cudaStreamSynchronize(s));
+        if (p == 0) st->retried = ovf_host;
+        if (ovf_host == 0) break;
+        q_items = ovf_items;
+        q_count = ovf_count;
+        queued = ovf_host;
+    }
+    if (ovf_host > 0) tc_launch_mark_capacity(q_items, ovf_host, out, s);
+    launch_status_reduce(out, n, small + SM_WORST, s);
+    int worst = 0;
+    unsigned long long vs = 0;
+    AMTC_CUDA(cudaMemcpyAsync(&worst, small + SM_WORST, sizeof(int), cudaMemcpyDeviceToHost, s));
+    AMTC_CUDA(cudaMemcpyAsync(&vs, small + SM_VSUM, sizeof(vs), cudaMemcpyDeviceToHost, s));
+    AMTC_CUDA(cudaStreamSynchronize(s));
+    AMTC_CUDA(cudaGetLastError());
+    st->vertex_sum = vs;
+    st->passes = passes;
+    st->solve_ms = 0.0;
+    for (int p = 0; p < passes; ++p) {
+        float ms = 0.f;
+        AMTC_CUDA(cudaEventElapsedTime(&ms, st->ev[2 * p], st->ev[2 * p + 1]));
+        st->solve_ms += ms;
+    }
+    return worst;
+}
+
+// host-pointer variants: stage through device buffers
+static size_t soa_bytes(int64_t n) { return (size_t)n * (7 * sizeof(double) + sizeof(int32_t)); }
+
+static int stage_in(DevState* st, const amtc_batch_soa* h, int64_t n, amtc_batch_soa* d, cudaStream_t s) {
+    cudaError_t e = st->stage_in.ensure(soa_bytes(n) + 64);
+    if (e != cudaSuccess) return cuda_fail(e, "stage_in");
+    char* base = static_cast<char*>(st->stage_in.p);
+    double* f = reinterpret_cast<double*>(base);
+    const double* src[7] = {h->S0, h->K, h->K2, h->T, h->sigma, h->R, h->k};
+    const double** dst[7] = {&d->S0, &d->K, &d->K2, &d->T, &d->sigma, &d->R, &d->k};
+    for (int a = 0; a < 7; ++a) {
+        if (src[a]) {
+            AMTC_CUDA(cudaMemcpyAsync(f + a * n, src[a], sizeof(double) * n, cudaMemcpyHostToDevice, s));
+            *dst[a] = f + a * n;
+        } else {
+            *dst[a] = nullptr;
+        }
+    }
+    int32_t* kd = reinterpret_cast<int32_t*>(f + 7 * n);
+    AMTC_CUDA(cudaMemcpyAsync(kd, h->kind, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    d->kind = kd;
+    return STATUS_OK;
+}
+
+}  // namespace amtc
+
+using namespace amtc;
+
+extern "C" {
+
+int amtc_price_american_tc_batch(const amtc_batch_soa* d_in, int64_t n, int32_t N, amtc_quote* d_out,
+                                 void* cuda_stream) {
+    try {
+        return tc_batch_device(d_in, n, N, d_out, static_cast<cudaStream_t>(cuda_stream));
+    } catch (...) {
+        g_last_error = "unexpected host exception";
+        return STATUS_ECUDA;
+    }
+}
+
+int amtc_price_american_tc_batch_host(const amtc_batch_soa* h_in, int64_t n, int32_t N, amtc_quote* h_out,
+                                      void* cuda_stream) {
+    try {
+        if (!soa_ok(h_in) || !h_out || n < 0 || N < 1) return STATUS_EINVAL;
+        if (n == 0) return STATUS_OK;
+        cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+        int dev = 0;
+        AMTC_CUDA(cudaGetDevice(&dev));
+        DevState* st = state_for_device(dev);
+        amtc_batch_soa d;
+        {
+            std::lock_guard<std::mutex> g(st->mu);
+            int rc = stage_in(st, h_in, n, &d, s);
+            if (rc) return rc;
+            AMTC_CUDA(st->stage_out.ensure(sizeof(amtc_quote) * (size_t)n));
+        }
+        amtc_quote* d_out = static_cast<amtc_quote*>(st->stage_out.p);
+        int rc = tc_batch_device(&d, n, N, d_out, s);
+        if (rc == STATUS_ECUDA) return rc;
+        AMTC_CUDA(cudaMemcpyAsync(h_out, d_out, sizeof(amtc_quote) * (size_t)n, cudaMemcpyDeviceToHost, s));
+        AMTC_CUDA(cudaStreamSynchronize(s));
+        return rc;
+    } catch (...) {
+        g_last_error = "unexpected host exception";
+        return STATUS_ECUDA;
+    }
+}
+
+amtc_quote amtc_price_american_tc(const amtc_params* params, int32_t N, const amtc_payoff* payoff, double k) {
+    amtc_quote q;
+    q.ask = NAN;
+    q.bid = NAN;
+    q.max_bp = 0;
+    if (!params || !payoff || payoff->flags != 0) {
+        q.status = STATUS_EINVAL;
+        return q;
+    }
+    double S0 = params->S0, K = payoff->K, K2 = payoff->K2, T = params->T, sg = params->sigma, R = params->R;
+    int32_t kind = payoff->kind;
+    amtc_batch_soa h;
+    h.S0 = &S0; h.K = &K; h.K2 = &K2; h.T = &T; h.sigma = &sg; h.R = &R; h.k = &k; h.kind = &kind;
+    int rc = amtc_price_american_tc_batch_host(&h, 1, N, &q, nullptr);
+    if (rc == STATUS_ECUDA || (rc == STATUS_EINVAL && N < 1)) q.status = rc;
+    return q;
+}
+
+int amtc_price_crr_batch(const amtc_batch_soa* d_in, int64_t n, int32_t N, double* d_price, void* cuda_stream) {
+    try {
+        if (!soa_ok(d_in) || !d_price || n < 0 || N < 1) return STATUS_EINVAL;
+        if (n == 0) return STATUS_OK;
+        if (N > crr_max_n()) {
+            g_last_error = "N exceeds the register-resident CRR kernel";
+            return STATUS_EINVAL;
+        }
+        int rc = crr_launch(to_ptrs(d_in), n, N, d_price, static_cast<cudaStream_t>(cuda_stream));
+        AMTC_CUDA(cudaGetLastError());
+        return rc;
+    } catch (...) {
+        g_last_error = "unexpected host exception";
+        return STATUS_ECUDA;
+    }
+}
+
+int amtc_price_crr_batch_host(const amtc_batch_soa* h_in, int64_t n, int32_t N, double* h_price,
+                              void* cuda_stream) {
+    try {
+        if (!soa_ok(h_in) || !h_price || n < 0 || N < 1) return STATUS_EINVAL;
+        if (n == 0) return STATUS_OK;
+        cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+        int dev = 0;
+        AMTC_CUDA(cudaGetDevice(&dev));
+        DevState* st = state_for_device(dev);
+        std::lock_guard<std::mutex> g(st->mu);
+        amtc_batch_soa d;
+        int rc = stage_in(st, h_in, n, &d, s);
+        if (rc) return rc;
+        AMTC_CUDA(st->stage_out.ensure(sizeof(double) * (size_t)n));
+        double* d_price = static_cast<double*>(st->stage_out.p);
+        rc = amtc_price_crr_batch(&d, n, N, d_price, s);
+        if (rc) return rc;
+        AMTC_CUDA(cudaMemcpyAsync(h_price, d_price, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, s));
+        AMTC_CUDA(cudaStreamSynchronize(s));
+        return STATUS_OK;
+    } catch (...) {
+        g_last_error = "unexpected host exception";
+        return STATUS_ECUDA;
+    }
+}
+
+const char* amtc_strerror(int status) {
+    switch (status) {
+        case STATUS_OK: return "AMTC_OK";
+        case STATUS_EINVAL: return "AMTC_EINVAL: invalid argument";
+        case STATUS_EARBITRAGE: return "AMTC_EARBITRAGE: calibration violates d < r < u";
+        case STATUS_ECAPACITY: return "AMTC_ECAPACITY: node function exceeded every scratch capacity";
+        case STATUS_EUNBOUNDED: return "AMTC_EUNBOUNDED: slope restriction unbounded below";
+        case STATUS_ECUDA: return "AMTC_ECUDA: CUDA runtime error";
+        case STATUS_ENCCL: return "AMTC_ENCCL: NCCL error";
+        default: return "AMTC: unknown status";
+    }
+}
+
+const char* amtc_last_error(void) { return g_last_error.c_str(); }
+
+int64_t amtc_launch_count(void) { return g_launches.load(); }
+
+int amtc_tc_last_stats(amtc_tc_stats* out) {
+    if (!out) return STATUS_EINVAL;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return STATUS_ECUDA;
+    DevState* st = state_for_device(dev);
+    std::lock_guard<std::mutex> g(st->mu);
+    out->vertex_sum = (int64_t)st->vertex_sum;
+    out->passes = st->passes;
+    out->retried_items = st->retried;
+    out->solve_ms = st->solve_ms;
+    return STATUS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,172 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the
+same seeded inputs.  Tolerance (north star): 1e-9 relative in fp64; prices
+below 1e-3 also accept an absolute 1e-12 (reading A19)."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1110_2477_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+RTOL, ATOL = 1e-9, 1e-12
+
+
+def close(g, o):
+    return abs(g - o) <= max(RTOL * abs(o), ATOL)
+
+
+@pytest.fixture(scope="module")
+def api():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_1110_2477_b200 import api as A
+    A.lib()
+    return A
+
+
+def _opt(row):
+    return O.Option(row["S0"], row["K"], row["T"], row["sigma"], row["R"], row["k"], row["kind"], row["K2"])
+
+
+def assert_quotes(got, batch, N, want=None):
+    want = want if want is not None else [O.price_tc(_opt(batch.row(i)), N) for i in range(len(batch))]
+    bad = []
+    for i, q in enumerate(want):
+        g = got[i]
+        assert g["status"] == q.status, (i, batch.row(i), g, q)
+        if q.status:
+            assert math.isnan(g["ask"]) and math.isnan(g["bid"])
+            continue
+        if not (close(g["ask"], q.ask) and close(g["bid"], q.bid)):
+            bad.append((i, batch.row(i), float(g["ask"]), q.ask, float(g["bid"]), q.bid))
+    assert not bad, bad[:5]
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 7, 33, 130])
+def test_tc_random_small(api, N):
+    b = W.random_small(48, seed=1000 + N, k_max=0.05)
+    got, rc = api.price_american_tc_batch_host(b, N)
+    assert rc == 0
+    assert_quotes(got, b, N)
+
+
+def test_tc_device_batch_matches_host(api):
+    import torch
+    b = W.random_small(40, seed=77)
+    cols = api.device_batch(b)
+    out, rc = api.price_american_tc_batch(cols, 60)
+    torch.cuda.synchronize()
+    dev = api.quotes_to_numpy(out)
+    host, rc2 = api.price_american_tc_batch_host(b, 60)
+    assert rc == rc2 == 0
+    np.testing.assert_array_equal(dev["ask"], host["ask"])
+    np.testing.assert_array_equal(dev["bid"], host["bid"])
+
+
+def test_config1_single_put(api):
+    """BASELINE config 1 through the north-star single-option call."""
+    for k in (0.005, 0.0):
+        q = api.price_american_tc(100.0, 100.0, 0.25, 0.2, 0.1, W.CONFIG1_N, k, api.PUT)
+        o = O.price_tc(O.Option(100.0, 100.0, 0.25, 0.2, 0.1, k, O.PUT), W.CONFIG1_N)
+        assert q["status"] == 0
+        assert close(q["ask"], o.ask) and close(q["bid"], o.bid), (q, o)
+    crr = O.price_crr(O.Option(100.0, 100.0, 0.25, 0.2, 0.1, 0.0, O.PUT), W.CONFIG1_N)
+    assert abs(q["ask"] - crr) <= 1e-9 * crr and abs(q["bid"] - crr) <= 1e-9 * crr
+
+
+def test_edge_cases(api):
+    # empty batch
+    empty = W.random_small(0, seed=1)
+    got, rc = api.price_american_tc_batch_host(empty, 10)
+    assert rc == 0 and len(got) == 0
+    # invalid / arbitrage options mixed with valid ones
+    b = W.random_small(6, seed=5)
+    b.S0[1] = -1.0
+    b.k[2] = 1.0
+    b.kind[3] = 9
+    b.sigma[4] = 1e-4  # h tiny -> r >= u at R > 0 ?
+    b.R[4] = 0.08
+    got, rc = api.price_american_tc_batch_host(b, 8)
+    assert got["status"][1] == 1 and got["status"][2] == 1 and got["status"][3] == 1
+    assert got["status"][4] == 2
+    assert rc == 2 or rc == 1
+    assert_quotes(got, b, 8)
+    # k = 0: lines only; equals CRR
+    b0 = W.random_small(16, seed=9, k_max=0.0)
+    got, rc = api.price_american_tc_batch_host(b0, 100)
+    for i in range(len(b0)):
+        crr = O.price_crr(_opt(b0.row(i)), 100)
+        assert close(got["ask"][i], crr) and close(got["bid"][i], crr)
+
+
+def test_config3_sweep(api):
+    """BASELINE config 3: put and call, k x N sweep, single trees."""
+    ref = json.load(open(os.path.join(GOLD, "oracle_config3.json")))["points"]
+    bad = []
+    for p in ref:
+        kind = p["kind"]
+        q = api.price_american_tc(100.0, 100.0, 1.0, 0.2, 0.05, p["N"], p["k"], kind)
+        assert q["status"] == 0, (p, q)
+        if not (close(q["ask"], p["ask"]) and close(q["bid"], p["bid"])):
+            bad.append((p, q))
+    assert not bad, bad[:3]
+
+
+def test_config4_full_batch_sampled(api):
+    """BASELINE config 4 at full size (16384 options, N=1500) in the bench's
+    launch configuration; sampled outputs against stored oracle values."""
+    import torch
+    ref = json.load(open(os.path.join(GOLD, "oracle_config4.json")))
+    b = W.config4()
+    cols = api.device_batch(b)
+    out, rc = api.price_american_tc_batch(cols, ref["N"])
+    torch.cuda.synchronize()
+    q = api.quotes_to_numpy(out)
+    assert rc == 0, api.STATUS[rc]
+    assert np.all(q["status"] == 0)
+    assert np.all(np.isfinite(q["ask"])) and np.all(np.isfinite(q["bid"]))
+    assert np.all(q["ask"] >= q["bid"] - 1e-12)
+    bad = []
+    for s in ref["samples"]:
+        g = q[s["index"]]
+        if not (close(g["ask"], s["ask"]) and close(g["bid"], s["bid"])):
+            bad.append((s, float(g["ask"]), float(g["bid"])))
+    assert not bad, bad[:3]
+
+
+def test_crr_config2_full_batch_sampled(api):
+    """BASELINE config 2 (65536 options, N=1024) full batch; sampled parity."""
+    import torch
+    ref = json.load(open(os.path.join(GOLD, "oracle_config2.json")))
+    b = W.config2()
+    cols = api.device_batch(b)
+    out = api.price_crr_batch(cols, ref["N"])
+    torch.cuda.synchronize()
+    v = out.cpu().numpy()
+    assert np.all(np.isfinite(v)) and np.all(v >= 0)
+    bad = [(s, v[s["index"]]) for s in ref["samples"] if not close(v[s["index"]], s["price"])]
+    assert not bad, bad[:3]
+
+
+@pytest.mark.parametrize("N", [1, 2, 127, 128, 129, 500, 1024, 1151])
+def test_crr_small_and_ragged(api, N):
+    b = W.random_small(37, seed=N)
+    got = api.price_crr_batch_host(b, N)
+    for i in range(len(b)):
+        o = O.price_crr(_opt(b.row(i)), N)
+        assert close(got[i], o), (i, N, got[i], o)
+
+
+def test_crr_equals_tc_at_k0(api):
+    b = W.random_small(24, seed=3, k_max=0.0)
+    N = 300
+    crr = api.price_crr_batch_host(b, N)
+    tc, rc = api.price_american_tc_batch_host(b, N)
+    assert rc == 0
+    np.testing.assert_allclose(tc["ask"], crr, rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(tc["bid"], crr, rtol=1e-9, atol=1e-12)
