@@ -89,10 +89,17 @@ static bool soa_ok(const amtc_batch_soa* b) {
 // small device scratch layout (ints)
 enum { SM_HIST = 0, SM_WORK = TC_CLASSES + 1, SM_OVF0, SM_OVF1, SM_WORST, SM_VSUM = 32, SM_INTS = 64 };
 
+// solver passes: the shared-memory solver (amtc_tc2.cu) first; items that
+// overflow its arenas are re-run with 4x arenas, then on the global-memory
+// solver (amtc_tc.cu) with growing scratch bounds.
 struct Pass {
-    int bmul, badd, cap_per_node;
+    int tc2;               // 1 = shared-memory solver
+    int bmul, badd;        // tc1: per-node scratch bound
+    int cap_per_node;      // tc1: arena vertices per node; tc2: big arena vertices per node
+    int heavy_per_node;    // tc2: warp scratch vertices per node
 };
-static const Pass kPasses[] = {{2, 8, 48}, {3, 16, 384}, {4, 32, 4096}, {8, 64, 32768}};
+static const Pass kPasses[] = {{1, 0, 0, 128, 96},  {1, 0, 0, 512, 192}, {0, 3, 16, 384, 0},
+                               {0, 4, 32, 4096, 0}, {0, 8, 64, 32768, 0}};
 
 static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amtc_quote* d_out,
                            cudaStream_t s) {
@@ -131,46 +138,80 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
     int ovf_host = 0;
     int passes = 0;
     const int n_passes = (int)(sizeof(kPasses) / sizeof(kPasses[0]));
+    const bool tc2_ok = N <= tc2_max_n() && tc2_pick_ks(N) > 0;
+    if (!st->ev[0]) {
+        for (auto& e : st->ev) AMTC_CUDA(cudaEventCreate(&e));
+    }
     for (int p = 0; p < n_passes; ++p) {
         const Pass& P = kPasses[p];
-        const int64_t cap64 = (int64_t)(N + 2) * P.cap_per_node;
-        const int arena_cap = (int)std::min<int64_t>(cap64, (int64_t)1 << 30);
-        const size_t wsb = (tc_workspace_bytes(N, arena_cap) + 255) & ~(size_t)255;
-        int64_t grid = (int64_t)st->sm_count * st->occupancy;
+        if (P.tc2 && !tc2_ok) continue;
+        size_t wsb;
+        int arena_cap = 0, big_cap = 0, heavy_scr = 0;
+        int64_t grid;
+        if (P.tc2) {
+            big_cap = (int)std::min<int64_t>((int64_t)(N + 2) * P.cap_per_node, (int64_t)1 << 28);
+            heavy_scr = (int)std::min<int64_t>((int64_t)(N + 2) * P.heavy_per_node + 4096, (int64_t)1 << 28);
+            wsb = (tc2_workspace_bytes(N, big_cap, heavy_scr) + 255) & ~(size_t)255;
+            grid = st->sm_count;  // one CTA per SM (the level fills shared memory)
+        } else {
+            arena_cap = (int)std::min<int64_t>((int64_t)(N + 2) * P.cap_per_node, (int64_t)1 << 30);
+            wsb = (tc_workspace_bytes(N, arena_cap) + 255) & ~(size_t)255;
+            grid = (int64_t)st->sm_count * st->occupancy;
+        }
         grid = std::min<int64_t>(grid, queued);
         grid = std::min<int64_t>(grid, (int64_t)(budget / wsb));
-        if (grid < 1) break;
+        if (grid < 1) continue;
         AMTC_CUDA(st->ws.ensure(wsb * (size_t)grid));
-        int* ovf_count = small + (p % 2 == 0 ? SM_OVF0 : SM_OVF1);
-        int* ovf_items = static_cast<int*>(st->items[(p + 1) % 2].p);
+        int* ovf_count = small + (passes % 2 == 0 ? SM_OVF0 : SM_OVF1);
+        int* ovf_items = static_cast<int*>(st->items[(passes + 1) % 2].p);
+        if (q_items == ovf_items) ovf_items = static_cast<int*>(st->items[passes % 2].p);
         AMTC_CUDA(cudaMemsetAsync(small + SM_WORK, 0, sizeof(int), s));
         AMTC_CUDA(cudaMemsetAsync(ovf_count, 0, sizeof(int), s));
-        if (!st->ev[0]) {
-            for (auto& e : st->ev) AMTC_CUDA(cudaEventCreate(&e));
+        AMTC_CUDA(cudaEventRecord(st->ev[2 * passes], s));
+        if (P.tc2) {
+            Tc2Launch L;
+            L.in = in;
+            L.N = N;
+            L.out = out;
+            L.items = q_items;
+            L.n_items = q_count;
+            L.work_counter = small + SM_WORK;
+            L.ovf_items = ovf_items;
+            L.ovf_count = ovf_count;
+            L.vertex_sum = reinterpret_cast<unsigned long long*>(small + SM_VSUM);
+            L.ws = static_cast<char*>(st->ws.p);
+            L.ws_stride = wsb;
+            L.big_cap = big_cap;
+            L.heavy_scr = heavy_scr;
+            int rc = tc2_launch(L, (int)grid, s);
+            if (rc) {
+                g_last_error = "tc2 launch failed";
+                return STATUS_ECUDA;
+            }
+        } else {
+            TcLaunch L;
+            L.in = in;
+            L.N = N;
+            L.out = out;
+            L.items = q_items;
+            L.n_items = q_count;
+            L.work_counter = small + SM_WORK;
+            L.ovf_items = ovf_items;
+            L.ovf_count = ovf_count;
+            L.vertex_sum = reinterpret_cast<unsigned long long*>(small + SM_VSUM);
+            L.ws = static_cast<char*>(st->ws.p);
+            L.ws_stride = wsb;
+            L.arena_cap = arena_cap;
+            L.bmul = P.bmul;
+            L.badd = P.badd;
+            tc_launch_solve(L, (int)grid, s);
         }
-        TcLaunch L;
-        L.in = in;
-        L.N = N;
-        L.out = out;
-        L.items = q_items;
-        L.n_items = q_count;
-        L.work_counter = small + SM_WORK;
-        L.ovf_items = ovf_items;
-        L.ovf_count = ovf_count;
-        L.vertex_sum = reinterpret_cast<unsigned long long*>(small + SM_VSUM);
-        L.ws = static_cast<char*>(st->ws.p);
-        L.ws_stride = wsb;
-        L.arena_cap = arena_cap;
-        L.bmul = P.bmul;
-        L.badd = P.badd;
-        AMTC_CUDA(cudaEventRecord(st->ev[2 * p], s));
-        tc_launch_solve(L, (int)grid, s);
         AMTC_CUDA(cudaGetLastError());
-        AMTC_CUDA(cudaEventRecord(st->ev[2 * p + 1], s));
+        AMTC_CUDA(cudaEventRecord(st->ev[2 * passes + 1], s));
         passes++;
         AMTC_CUDA(cudaMemcpyAsync(&ovf_host, ovf_count, sizeof(int), cudaMemcpyDeviceToHost, s));
         AMTC_CUDA(cudaStreamSynchronize(s));
-        if (p == 0) st->retried = ovf_host;
+        if (passes == 1) st->retried = ovf_host;
         if (ovf_host == 0) break;
         q_items = ovf_items;
         q_count = ovf_count;

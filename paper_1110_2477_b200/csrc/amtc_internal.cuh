@@ -66,6 +66,27 @@ void tc_launch_solve(const TcLaunch& L, int grid, cudaStream_t s);
 void tc_launch_mark_capacity(const int* items, int n_items, Quote* out, cudaStream_t s);
 int tc_solve_occupancy();
 
+// amtc_tc2.cu (shared-memory solver)
+struct Tc2Launch {
+    BatchPtrs in;
+    int N;
+    Quote* out;
+    const int* items;
+    const int* n_items;
+    int* work_counter;
+    int* ovf_items;
+    int* ovf_count;
+    unsigned long long* vertex_sum;
+    char* ws;
+    size_t ws_stride;
+    int big_cap;    // vertices per big arena (two per CTA)
+    int heavy_scr;  // vertices of warp-cooperative scratch per warp
+};
+size_t tc2_workspace_bytes(int N, int big_cap, int heavy_scr);
+int tc2_launch(const Tc2Launch& L, int grid, cudaStream_t s);
+int tc2_max_n();
+int tc2_pick_ks(int N);
+
 // amtc_crr.cu
 int crr_launch(const BatchPtrs& in, int64_t n, int N, double* out, cudaStream_t s);
 int crr_max_n();

@@ -230,40 +230,20 @@ __global__ void __launch_bounds__(TC_THREADS) tc_solve_kernel(TcLaunch L) {
                 const double lo = -kp * S * disc, hi = -km * S * disc;  // [-S^a, -S^b] r^-t
                 Fn U{A0 + off[cur][j], cc[j], slb[cur][j]};
                 Fn D{A0 + off[cur][j + 1], cc[j + 1], slb[cur][j + 1]};
-                // w = max(z^u, z^d)  (discounted: no division by r)
-                Emit E;
-                E.out = r0; E.cap = b;
-                envelope(U, D, true, E);
-                err |= E.err;
-                Fn W{r0, E.m, E.sl};
-                // v = restriction of w to [lo, hi]  (reading R7)
-                int nA; double slA;
-                err |= restrict_pass_a(W, lo, r1, b, nA, slA);
-                if (err) break;
-                Fn Af{r1 + (b - nA), nA, slA};
-                Emit EV;
-                EV.out = r0; EV.cap = b;
-                err |= restrict_pass_b(Af, hi, EV);
-                if (err) break;
-                Fn Vf{r0, EV.m, EV.sl};
                 // u_t: seller Eq.(1), buyer Eq.(6) P:133 (discounted)
                 double xi, zeta;
                 payoff(oc, S, xi, zeta);
-                Vtx uv;
-                uv.x = party == 0 ? zeta : -zeta;
-                uv.f = (party == 0 ? xi : -xi) * disc;
-                uv.s = hi;
-                Fn Uf{&uv, 1, lo};
-                // z = max(u, v) seller / min(u, v) buyer
-                Emit EZ;
-                EZ.out = r1; EZ.cap = b;
-                envelope(Uf, Vf, party == 0, EZ);
-                err |= EZ.err;
-                cnt[nxt][j] = EZ.m;
+                const double ux = party == 0 ? zeta : -zeta;
+                const double uf = (party == 0 ? xi : -xi) * disc;
+                int nZ;
+                double slZ;
+                err |= node_update(U, D, lo, hi, ux, uf, party == 0, r0, r1, b, nZ, slZ);
+                if (err) break;
+                cnt[nxt][j] = nZ;
                 off[nxt][j] = (int)(r1 - A1);
-                slb[nxt][j] = EZ.sl;
-                my_vertices += (unsigned long long)EZ.m;
-                if (EZ.m > 1) atomicMax(&s_maxn, EZ.m);
+                slb[nxt][j] = slZ;
+                my_vertices += (unsigned long long)nZ;
+                if (nZ > 1) atomicMax(&s_maxn, nZ);
             }
             if (err) atomicOr(&s_err, err);
             __syncthreads();

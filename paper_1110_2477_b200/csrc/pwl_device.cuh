@@ -17,7 +17,14 @@
 // restriction to [-S^a_t r^-t, -S^b_t r^-t] (restriction commutes with
 // positive scaling).  At t = 0, r^0 = 1, so prices read off unchanged.
 #pragma once
+#include <cmath>
 #include <cstdint>
+
+#ifdef __CUDACC__
+#define AMTC_HD __host__ __device__ __forceinline__
+#else
+#define AMTC_HD inline
+#endif
 
 namespace amtc {
 
@@ -27,6 +34,16 @@ struct Vtx {
 
 // status bits raised by the device algebra
 enum : int { DEV_OK = 0, DEV_OVERFLOW = 1, DEV_UNBOUNDED = 2 };
+
+// Rounding guards (reading R10: they change values by rounding-level amounts
+// only and keep the representation free of rounding-made micro-pieces):
+//  * two values closer than TOL_F (|a| + |b| + 1) are "equal": a function does
+//    not "cross" another it merely touches (ties are broken by slope);
+//  * a piece shorter than TOL_X (1 + |x|) is folded into its neighbour.
+constexpr double TOL_F = 1e-14;
+constexpr double TOL_X = 1e-12;
+AMTC_HD double ftol(double a, double b) { return TOL_F * (fabs(a) + fabs(b) + 1.0); }
+AMTC_HD double xtol(double x) { return TOL_X * (1.0 + fabs(x)); }
 
 // Forward emitter: appends vertices in increasing x, skipping non-kinks
 // (same slope as the previous piece) and folding zero-length pieces.
@@ -39,15 +56,15 @@ struct Emit {
     bool has_anchor;
     int err;
 
-    __device__ __forceinline__ void init(Vtx* o, int c, double left_slope) {
+    AMTC_HD void init(Vtx* o, int c, double left_slope) {
         out = o; m = 0; cap = c; sl = left_slope; last_s = left_slope; has_anchor = false; err = DEV_OK;
     }
-    __device__ __forceinline__ void push(double x, double f, double s) {
+    AMTC_HD void push(double x, double f, double s) {
         if (!has_anchor) { ax = x; af = f; has_anchor = true; }
         if (s == last_s) return;  // not a kink
-        if (m > 0 && !(x > out[m - 1].x)) {
-            // zero-length piece (coincident or rounding-reversed vertex): the
-            // previous vertex turns directly into slope s
+        if (m > 0 && !(x > out[m - 1].x + xtol(x))) {
+            // (near) zero-length piece (coincident or rounding-made vertex):
+            // the previous vertex turns directly into slope s
             out[m - 1].s = s;
             double left = (m > 1) ? out[m - 2].s : sl;
             if (left == s) m--;  // the previous vertex is no longer a kink
@@ -60,7 +77,7 @@ struct Emit {
         last_s = s;
     }
     // close the function: a line keeps one anchor vertex
-    __device__ __forceinline__ int finish() {
+    AMTC_HD int finish() {
         if (m == 0) {
             if (cap < 1) { err |= DEV_OVERFLOW; return 0; }
             out[0].x = has_anchor ? ax : 0.0;
@@ -77,12 +94,12 @@ struct Fn {
     const Vtx* v;
     int n;
     double sl;
-    __device__ __forceinline__ double slope_right(int i) const { return i < 0 ? sl : v[i].s; }
+    AMTC_HD double slope_right(int i) const { return i < 0 ? sl : v[i].s; }
 };
 
 // value at y of the piece that starts at vertex i (i = -1: the left tail,
 // anchored at vertex 0)
-__device__ __forceinline__ double piece_at(const Fn& F, int i, double y) {
+AMTC_HD double piece_at(const Fn& F, int i, double y) {
     const Vtx& a = F.v[i < 0 ? 0 : i];
     double s = i < 0 ? F.sl : a.s;
     return fma(s, y - a.x, a.f);
@@ -92,13 +109,14 @@ __device__ __forceinline__ double piece_at(const Fn& F, int i, double y) {
 // z = max(u, v); P:142 z = min(u, v)).  A two-pointer sweep over the union of
 // both vertex sets; between consecutive events both are affine, so at most one
 // crossing per interval (and per tail).
-__device__ __forceinline__ int envelope(const Fn& F, const Fn& G, bool is_max, Emit& E) {
+AMTC_HD int envelope(const Fn& F, const Fn& G, bool is_max, Emit& E) {
     // winner on the left tail
     double xe0 = fmin(F.v[0].x, G.v[0].x);
     double eF0 = piece_at(F, -1, xe0), eG0 = piece_at(G, -1, xe0);
     bool curF;
     if (F.sl != G.sl) curF = is_max ? (F.sl < G.sl) : (F.sl > G.sl);
     else curF = is_max ? (eF0 >= eG0) : (eF0 <= eG0);
+    // a left-tail winner that is only tied at the first event does not cross
     E.init(E.out, E.cap, curF ? F.sl : G.sl);
     int iF = -1, iG = -1;
     double sF = F.sl, sG = G.sl;
@@ -111,7 +129,8 @@ __device__ __forceinline__ int envelope(const Fn& F, const Fn& G, bool is_max, E
         eF = (xF == xe) ? F.v[iF + 1].f : piece_at(F, iF, xe);
         eG = (xG == xe) ? G.v[iG + 1].f : piece_at(G, iG, xe);
         // crossing inside (xprev, xe): the current winner lost strictly at xe
-        bool lost = curF ? (is_max ? (eG > eF) : (eG < eF)) : (is_max ? (eF > eG) : (eF < eG));
+        const double tl = ftol(eF, eG);
+        bool lost = curF ? (is_max ? (eG > eF + tl) : (eG < eF - tl)) : (is_max ? (eF > eG + tl) : (eF < eG - tl));
         if (lost) {
             // sF == sG only if rounding flipped the order of parallel lines
             double yc = (sF != sG) ? xe - (eF - eG) / (sF - sG) : xe;
@@ -122,8 +141,8 @@ __device__ __forceinline__ int envelope(const Fn& F, const Fn& G, bool is_max, E
         }
         if (xF == xe) { iF++; sF = F.v[iF].s; }
         if (xG == xe) { iG++; sG = G.v[iG].s; }
-        if (eF != eG) curF = is_max ? (eF > eG) : (eF < eG);
-        else curF = is_max ? (sF >= sG) : (sF <= sG);
+        if (fabs(eF - eG) > tl) curF = is_max ? (eF > eG) : (eF < eG);
+        else curF = is_max ? (sF >= sG) : (sF <= sG);  // tie: the one that wins to the right
         E.push(xe, is_max ? fmax(eF, eG) : fmin(eF, eG), curF ? sF : sG);
         xprev = xe;
     }
@@ -149,12 +168,11 @@ struct EmitRev {
     Vtx* out;
     int m, cap;
     int err;
-    __device__ __forceinline__ void init(Vtx* o, int c) { out = o; m = 0; cap = c; err = DEV_OK; }
-    __device__ __forceinline__ void push(double x, double f, double s_right) {
+    AMTC_HD void init(Vtx* o, int c) { out = o; m = 0; cap = c; err = DEV_OK; }
+    AMTC_HD void push(double x, double f, double s_right) {
         if (m > 0) {
             Vtx& last = out[cap - m];  // the vertex to the right
-            if (!(x < last.x)) {       // zero-length piece: fold into the right vertex
-                last.f = f;
+            if (!(x < last.x - xtol(x))) {  // (near) zero-length piece: fold into the right vertex
                 return;
             }
         }
@@ -175,7 +193,7 @@ struct EmitRev {
 // line of slope lo / hi ("flat"), switching at vertices or single crossings.
 //
 // Pass A writes A reversed into `abuf` (cap entries, the last nA used).
-__device__ __forceinline__ int restrict_pass_a(const Fn& W, double lo, Vtx* abuf, int cap, int& nA,
+AMTC_HD int restrict_pass_a(const Fn& W, double lo, Vtx* abuf, int cap, int& nA,
                                                double& slA) {
     EmitRev R;
     R.init(abuf, cap);
@@ -201,7 +219,7 @@ __device__ __forceinline__ int restrict_pass_a(const Fn& W, double lo, Vtx* abuf
             s_left = lo;
             if (sp > lo) {
                 double d = fw - Ax;
-                if (d <= 0.0) {  // W touches the flat line at x: track from here
+                if (d <= ftol(fw, Ax)) {  // W touches the flat line at x: track from here
                     flat = false; Ax = fw; s_left = sp;
                 } else {
                     yc = x - d / (sp - lo);
@@ -229,7 +247,7 @@ __device__ __forceinline__ int restrict_pass_a(const Fn& W, double lo, Vtx* abuf
 }
 
 // Pass B over A (forward), emitting V through E (whose left slope is A's).
-__device__ __forceinline__ int restrict_pass_b(const Fn& A, double hi, Emit& E) {
+AMTC_HD int restrict_pass_b(const Fn& A, double hi, Emit& E) {
     if (A.sl > hi) return DEV_UNBOUNDED;
     E.init(E.out, E.cap, A.sl);
     bool flat = false;
@@ -251,7 +269,7 @@ __device__ __forceinline__ int restrict_pass_b(const Fn& A, double hi, Emit& E) 
             s_right = hi;
             if (sp < hi) {
                 double d = fa - Bx;
-                if (d <= 0.0) {
+                if (d <= ftol(fa, Bx)) {
                     flat = false; Bx = fa; s_right = sp;
                 } else {
                     yc = x + d / (hi - sp);
@@ -270,6 +288,53 @@ __device__ __forceinline__ int restrict_pass_b(const Fn& A, double hi, Emit& E) 
     }
     E.finish();
     return E.err;
+}
+
+}  // namespace amtc
+
+namespace amtc {
+
+// One node of the seller (party 0) or buyer (party 1)
+// recursion on discounted functions.  U, D: the children z_{t+1,j},
+// z_{t+1,j+1}; [lo, hi] = [-S^a_t, -S^b_t] r^-t; (ux, uf): the vertex of the
+// discounted exercise function u_t (seller: (zeta, xi r^-t), buyer:
+// (-zeta, -xi r^-t)) whose tails are lo and hi.
+// Scratch: r0 and r1, b vertices each.  The result Z is left in r1[0..nZ).
+AMTC_HD int node_update(const Fn& U, const Fn& D, double lo, double hi, double ux, double uf, bool seller,
+                        Vtx* r0, Vtx* r1, int b, int& nZ, double& slZ) {
+    // w = max(z^u, z^d)  (discounted, so no division by r)
+    Emit E;
+    E.out = r0;
+    E.cap = b;
+    envelope(U, D, true, E);
+    int err = E.err;
+    if (err) return err;
+    Fn W{r0, E.m, E.sl};
+    // v = restriction of w to [lo, hi]  (reading R7)
+    int nA;
+    double slA;
+    err |= restrict_pass_a(W, lo, r1, b, nA, slA);
+    if (err) return err;
+    Fn Af{r1 + (b - nA), nA, slA};
+    Emit EV;
+    EV.out = r0;
+    EV.cap = b;
+    err |= restrict_pass_b(Af, hi, EV);
+    if (err) return err;
+    Fn Vf{r0, EV.m, EV.sl};
+    // z = max(u, v) seller / min(u, v) buyer
+    Vtx uv;
+    uv.x = ux;
+    uv.f = uf;
+    uv.s = hi;
+    Fn Uf{&uv, 1, lo};
+    Emit EZ;
+    EZ.out = r1;
+    EZ.cap = b;
+    envelope(Uf, Vf, seller, EZ);
+    nZ = EZ.m;
+    slZ = EZ.sl;
+    return EZ.err;
 }
 
 }  // namespace amtc

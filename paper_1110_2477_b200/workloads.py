@@ -50,9 +50,9 @@ class Batch:
 
 def _batch(S0, K, K2, T, sigma, R, k, kind) -> Batch:
     n = len(K)
-    f = lambda a: np.ascontiguousarray(np.broadcast_to(np.asarray(a, dtype=np.float64), (n,)))
+    f = lambda a: np.array(np.broadcast_to(np.asarray(a, dtype=np.float64), (n,)), copy=True)
     return Batch(f(S0), f(K), f(K2), f(T), f(sigma), f(R), f(k),
-                 np.ascontiguousarray(np.broadcast_to(np.asarray(kind, dtype=np.int32), (n,))))
+                 np.array(np.broadcast_to(np.asarray(kind, dtype=np.int32), (n,)), copy=True))
 
 
 def config1(k: float = 0.005) -> Batch:
