@@ -18,7 +18,6 @@
 
 #include "amtc.h"
 #include "amtc_internal.cuh"
-#include "pwl_device.cuh"
 
 namespace amtc {
 
@@ -89,17 +88,10 @@ static bool soa_ok(const amtc_batch_soa* b) {
 // small device scratch layout (ints)
 enum { SM_HIST = 0, SM_WORK = TC_CLASSES + 1, SM_OVF0, SM_OVF1, SM_WORST, SM_VSUM = 32, SM_INTS = 64 };
 
-// solver passes: the shared-memory solver (amtc_tc2.cu) first; items that
-// overflow its arenas are re-run with 4x arenas, then on the global-memory
-// solver (amtc_tc.cu) with growing scratch bounds.
-struct Pass {
-    int tc2;               // 1 = shared-memory solver
-    int bmul, badd;        // tc1: per-node scratch bound
-    int cap_per_node;      // tc1: arena vertices per node; tc2: big arena vertices per node
-    int heavy_per_node;    // tc2: warp scratch vertices per node
-};
-static const Pass kPasses[] = {{1, 0, 0, 128, 96},  {1, 0, 0, 512, 192}, {0, 3, 16, 384, 0},
-                               {0, 4, 32, 4096, 0}, {0, 8, 64, 32768, 0}};
+// solver passes: every item first runs at capacity level 0; items that
+// overflowed a capacity (arena, scratch) are re-run at the next level (4x the
+// arenas, fewer concurrent warps), up to kMaxLevel; then ECAPACITY.
+constexpr int kMaxLevel = 4;
 
 static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amtc_quote* d_out,
                            cudaStream_t s) {
@@ -112,7 +104,11 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
     std::lock_guard<std::mutex> guard(st->mu);
     if (!st->sm_count) {
         AMTC_CUDA(cudaDeviceGetAttribute(&st->sm_count, cudaDevAttrMultiProcessorCount, dev));
-        st->occupancy = tc_solve_occupancy();
+        st->occupancy = strip_ctas_per_sm();
+        if (st->occupancy < 1) {
+            g_last_error = "strip solver cannot be resident on this device";
+            return STATUS_ECUDA;
+        }
     }
     const int64_t n2 = 2 * n;
     AMTC_CUDA(st->items[0].ensure(sizeof(int) * n2));
@@ -137,76 +133,38 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
     int64_t queued = n2;                                // upper bound for grid sizing
     int ovf_host = 0;
     int passes = 0;
-    const int n_passes = (int)(sizeof(kPasses) / sizeof(kPasses[0]));
-    const bool tc2_ok = N <= tc2_max_n() && tc2_pick_ks(N) > 0;
+    const int wpc = strip_warps_per_cta();
     if (!st->ev[0]) {
         for (auto& e : st->ev) AMTC_CUDA(cudaEventCreate(&e));
     }
-    for (int p = 0; p < n_passes; ++p) {
-        const Pass& P = kPasses[p];
-        if (P.tc2 && !tc2_ok) continue;
-        size_t wsb;
-        int arena_cap = 0, big_cap = 0, heavy_scr = 0;
-        int64_t grid;
-        if (P.tc2) {
-            big_cap = (int)std::min<int64_t>((int64_t)(N + 2) * P.cap_per_node, (int64_t)1 << 28);
-            heavy_scr = (int)std::min<int64_t>((int64_t)(N + 2) * P.heavy_per_node + 4096, (int64_t)1 << 28);
-            wsb = (tc2_workspace_bytes(N, big_cap, heavy_scr) + 255) & ~(size_t)255;
-            grid = st->sm_count;  // one CTA per SM (the level fills shared memory)
-        } else {
-            arena_cap = (int)std::min<int64_t>((int64_t)(N + 2) * P.cap_per_node, (int64_t)1 << 30);
-            wsb = (tc_workspace_bytes(N, arena_cap) + 255) & ~(size_t)255;
-            grid = (int64_t)st->sm_count * st->occupancy;
-        }
-        grid = std::min<int64_t>(grid, queued);
-        grid = std::min<int64_t>(grid, (int64_t)(budget / wsb));
-        if (grid < 1) continue;
-        AMTC_CUDA(st->ws.ensure(wsb * (size_t)grid));
+    for (int level = 0; level <= kMaxLevel; ++level) {
+        const size_t wsb = strip_ws_bytes_per_warp(N, level);
+        int64_t ctas = (int64_t)st->sm_count * st->occupancy;
+        ctas = std::min<int64_t>(ctas, (queued + wpc - 1) / wpc);
+        ctas = std::min<int64_t>(ctas, (int64_t)(budget / (wsb * wpc)));
+        if (ctas < 1) break;
+        AMTC_CUDA(st->ws.ensure(wsb * wpc * (size_t)ctas));
         int* ovf_count = small + (passes % 2 == 0 ? SM_OVF0 : SM_OVF1);
         int* ovf_items = static_cast<int*>(st->items[(passes + 1) % 2].p);
         if (q_items == ovf_items) ovf_items = static_cast<int*>(st->items[passes % 2].p);
         AMTC_CUDA(cudaMemsetAsync(small + SM_WORK, 0, sizeof(int), s));
         AMTC_CUDA(cudaMemsetAsync(ovf_count, 0, sizeof(int), s));
         AMTC_CUDA(cudaEventRecord(st->ev[2 * passes], s));
-        if (P.tc2) {
-            Tc2Launch L;
-            L.in = in;
-            L.N = N;
-            L.out = out;
-            L.items = q_items;
-            L.n_items = q_count;
-            L.work_counter = small + SM_WORK;
-            L.ovf_items = ovf_items;
-            L.ovf_count = ovf_count;
-            L.vertex_sum = reinterpret_cast<unsigned long long*>(small + SM_VSUM);
-            L.ws = static_cast<char*>(st->ws.p);
-            L.ws_stride = wsb;
-            L.big_cap = big_cap;
-            L.heavy_scr = heavy_scr;
-            int rc = tc2_launch(L, (int)grid, s);
-            if (rc) {
-                g_last_error = "tc2 launch failed";
-                return STATUS_ECUDA;
-            }
-        } else {
-            TcLaunch L;
-            L.in = in;
-            L.N = N;
-            L.out = out;
-            L.items = q_items;
-            L.n_items = q_count;
-            L.work_counter = small + SM_WORK;
-            L.ovf_items = ovf_items;
-            L.ovf_count = ovf_count;
-            L.vertex_sum = reinterpret_cast<unsigned long long*>(small + SM_VSUM);
-            L.ws = static_cast<char*>(st->ws.p);
-            L.ws_stride = wsb;
-            L.arena_cap = arena_cap;
-            L.bmul = P.bmul;
-            L.badd = P.badd;
-            tc_launch_solve(L, (int)grid, s);
-        }
-        AMTC_CUDA(cudaGetLastError());
+        StripLaunchArgs A;
+        A.in = in;
+        A.N = N;
+        A.out = out;
+        A.items = q_items;
+        A.n_items = q_count;
+        A.work_counter = small + SM_WORK;
+        A.ovf_items = ovf_items;
+        A.ovf_count = ovf_count;
+        A.vertex_sum = reinterpret_cast<unsigned long long*>(small + SM_VSUM);
+        A.ws = static_cast<char*>(st->ws.p);
+        A.ws_stride = wsb;
+        A.level = level;
+        A.ctas = (int)ctas;
+        if (strip_launch(A, s) != STATUS_OK) return cuda_fail(cudaGetLastError(), "strip_kernel launch");
         AMTC_CUDA(cudaEventRecord(st->ev[2 * passes + 1], s));
         passes++;
         AMTC_CUDA(cudaMemcpyAsync(&ovf_host, ovf_count, sizeof(int), cudaMemcpyDeviceToHost, s));

@@ -1,0 +1,102 @@
+// amtc_prepare.cu -- batch preparation for the transaction-cost solver:
+// per-option validation (SURVEY 8(b) error conventions), output
+// initialisation (NaN prices), and the heavy-first work queue of items
+// (option, party) for the persistent solver (longest-processing-time order:
+// the buyer of a call / bull spread at large k/h grows the long "sawtooth"
+// node functions).
+#include <cuda_runtime.h>
+
+#include "amtc_internal.cuh"
+#include "amtc_option.cuh"
+
+namespace amtc {
+
+// ---------------------------------------------------------------------------
+// prepare: validate, initialise quotes, order items heavy-first
+// ---------------------------------------------------------------------------
+constexpr int N_CLASSES = TC_CLASSES;
+
+// cost class of an item: the buyer of a call / bull spread grows "teeth" when
+// k/h is large (breakpoint counts measured with the oracle), so
+// those items are scheduled first (longest-processing-time order)
+__device__ __forceinline__ int item_class(const OptionConsts& oc, int party) {
+    if (party == 0 || oc.kind == KIND_PUT) return 0;
+    double kh = oc.k / oc.h;
+    return min(N_CLASSES - 1, 1 + (int)(4.0 * kh));
+}
+
+__global__ void tc_prepare_kernel(BatchPtrs in, int64_t n, int N, Quote* out, unsigned char* cls,
+                                  int* hist) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    OptionConsts oc;
+    int st = validate_option(in, i, N, true, oc);
+    out[i].ask = NAN;
+    out[i].bid = NAN;
+    out[i].status = st;
+    out[i].max_bp = 0;
+    for (int p = 0; p < 2; ++p) {
+        int c = (st == STATUS_OK) ? item_class(oc, p) : 255;
+        cls[2 * i + p] = (unsigned char)c;
+        if (c != 255) atomicAdd(&hist[c], 1);
+    }
+}
+
+// hist[c] -> start offset of class c in heavy-first order; hist[N_CLASSES] = total
+__global__ void tc_order_kernel(int* hist) {
+    if (threadIdx.x != 0) return;
+    int acc = 0;
+    for (int c = N_CLASSES - 1; c >= 0; --c) {
+        int v = hist[c];
+        hist[c] = acc;
+        acc += v;
+    }
+    hist[N_CLASSES] = acc;
+}
+
+__global__ void tc_scatter_kernel(int64_t n2, const unsigned char* cls, int* hist, int* items) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n2) return;
+    int c = cls[i];
+    if (c == 255) return;
+    int pos = atomicAdd(&hist[c], 1);
+    items[pos] = (int)i;
+}
+
+__global__ void status_reduce_kernel(const Quote* out, int64_t n, int* worst) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n && out[i].status) atomicMax(worst, out[i].status);
+}
+
+void launch_status_reduce(const Quote* out, int64_t n, int* worst, cudaStream_t s) {
+    cudaMemsetAsync(worst, 0, sizeof(int), s);
+    status_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(out, n, worst);
+    note_launch();
+}
+
+// mark items that exhausted every capacity
+__global__ void tc_mark_capacity_kernel(const int* items, int n_items, Quote* out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_items) return;
+    atomicMax(&out[items[i] >> 1].status, STATUS_ECAPACITY);
+}
+
+void tc_launch_prepare(const BatchPtrs& in, int64_t n, int N, Quote* out, unsigned char* cls, int* hist,
+                       int* items, cudaStream_t s) {
+    const int threads = 256;
+    cudaMemsetAsync(hist, 0, sizeof(int) * (N_CLASSES + 1), s);
+    tc_prepare_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(in, n, N, out, cls, hist);
+    note_launch();
+    tc_order_kernel<<<1, 32, 0, s>>>(hist);
+    note_launch();
+    tc_scatter_kernel<<<(unsigned)((2 * n + threads - 1) / threads), threads, 0, s>>>(2 * n, cls, hist, items);
+    note_launch();
+}
+
+void tc_launch_mark_capacity(const int* items, int n_items, Quote* out, cudaStream_t s) {
+    if (n_items <= 0) return;
+    tc_mark_capacity_kernel<<<(n_items + 255) / 256, 256, 0, s>>>(items, n_items, out);
+    note_launch();
+}
+
+}  // namespace amtc

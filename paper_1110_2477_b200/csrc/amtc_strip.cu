@@ -1,0 +1,470 @@
+// amtc_strip.cu -- the batched transaction-cost solver: one warp per work item
+// (option, party), the recombining tree swept in vertical strips.
+//
+// Recursion (Sec. 3; tree of Sec. 4.1): node (t, j)
+// needs only its children (t+1, j) and (t+1, j+1), so the dependency cone of a
+// node points to the RIGHT (larger j), as the paper's region-B argument notes
+// (P:164-166).  The warp therefore covers the triangle in strips of 32 columns,
+// right to left:
+//
+//   strip s owns columns j = 32 s + lane; it sweeps levels t = N .. max(32 s, 1)
+//   (lane active iff j <= t).  Lane l's up child (t+1, j) is its own previous
+//   result; the down child (t+1, j+1) is lane l+1's previous result, and for
+//   lane 31 the column 32 (s+1) of the strip to the right -- the "carry"
+//   column, written by that strip's lane 0 at every level (one function per
+//   level, in global memory: the only per-level traffic that leaves the SM).
+//   The leaves (t = N+1, payoff (0,0)) are analytic.
+//
+// This replaces the paper's p-thread block/region rounds (Alg. 1):
+// the GPU analogue of its region-B dependency is the carry column; there are
+// no barriers beyond __syncwarp, and no level is ever materialised in HBM.
+//
+// Node functions: a function is a vertex list
+// (x, f, s_right) with its left-tail slope carried alongside (pwl_device.cuh);
+// every function is stored discounted to t = 0 (z_t / r^t), so the paper's
+// w_t / r is a plain max.  Storage:
+//   * row slots: C vertices per lane, in shared memory, lane-interleaved
+//     (vertex i of lane l at row[i * 32 + l]: conflict-free for any mix of i);
+//   * functions with more than C vertices live in a per-warp global "row
+//     arena" (ping-pong by level parity) -- the heavy "sawtooth" of the buyer
+//     of calls / bull spreads;
+//   * node-update scratch: B vertices x 2 buffers per lane in shared memory;
+//     a node that outgrows it re-runs with per-lane global scratch (tier 2);
+//   * nodes whose children hold more than TL vertices in total are updated by
+//     the whole warp cooperatively (pwl_warp.cuh, tier 3).
+// Any capacity overflow aborts the item; the host re-runs it with larger
+// arenas (amtc_capi.cu), never truncating a function.
+#include <cuda_runtime.h>
+
+#include "amtc_internal.cuh"
+#include "amtc_option.cuh"
+#include "pwl_device.cuh"
+#include "pwl_lane.cuh"
+#include "pwl_warp.cuh"
+
+namespace amtc {
+
+constexpr int SW = 32;  // strip width = lanes per warp
+
+// per-warp global workspace: byte offsets of its regions (the second copy of
+// a ping-pong pair sits at offset + *_ps); computed once on the host
+struct StripLayout {
+    size_t epow, dpow;          // 2N+3 / N+2 doubles: e^{h (i-(N+1))}, e^{-rho t}
+    size_t chdr, csl, cv;       // carry column: header (n, arena offset | -1), left slope, C inline vertices
+    size_t carena, rarena;      // carry arena (per strip parity), row arena (per level parity)
+    size_t lscr, hscr;          // tier-2 lane scratch (32 x 2 x BG), tier-3 warp scratch
+    size_t chdr_ps, csl_ps, cv_ps, carena_ps, rarena_ps;
+    size_t total;
+};
+
+struct StripCaps {
+    int C, B, BG, TL;
+    int carena_cap, rarena_cap, hscr_cap;
+};
+
+__host__ __device__ inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+static StripLayout strip_layout(int N, const StripCaps& c) {
+    StripLayout L;
+    const size_t nn = (size_t)N + 2;
+    size_t p = 0;
+    auto take = [&](size_t bytes) { size_t q = p; p += align256(bytes); return q; };
+    L.epow = take(sizeof(double) * (2 * (size_t)N + 3));
+    L.dpow = take(sizeof(double) * nn);
+    L.chdr_ps = align256(sizeof(int2) * nn);
+    L.chdr = take(2 * L.chdr_ps);
+    L.csl_ps = align256(sizeof(double) * nn);
+    L.csl = take(2 * L.csl_ps);
+    L.cv_ps = align256(sizeof(Vtx) * nn * c.C);
+    L.cv = take(2 * L.cv_ps);
+    L.carena_ps = align256(sizeof(Vtx) * (size_t)c.carena_cap);
+    L.carena = take(2 * L.carena_ps);
+    L.rarena_ps = align256(sizeof(Vtx) * (size_t)c.rarena_cap);
+    L.rarena = take(2 * L.rarena_ps);
+    L.lscr = take(sizeof(Vtx) * (size_t)SW * 2 * c.BG);
+    L.hscr = take(sizeof(Vtx) * (size_t)c.hscr_cap);
+    L.total = p;
+    return L;
+}
+
+// per-warp shared memory
+template <int C, int B>
+struct StripSmem {
+    Vtx row[C * SW];  // lane-interleaved slots: vertex i of lane l at row[i * 32 + l]
+    Vtx s0[B * SW];   // lane-interleaved scratch of the node update (A of pass 1)
+    Vtx leaf31;       // lane 31's down child at t = N (an analytic leaf)
+    int rcnt[2];      // row arena bump counters
+    int ccnt;         // carry arena bump counter (current strip)
+    int pad;
+};
+
+struct StripLaunch {
+    BatchPtrs in;
+    int N;
+    Quote* out;
+    const int* items;
+    const int* n_items;
+    int* work_counter;
+    int* ovf_items;
+    int* ovf_count;
+    unsigned long long* vertex_sum;
+    char* ws;
+    StripCaps caps;
+    StripLayout lay;
+};
+
+#define WS(T, field, q) reinterpret_cast<T*>(wb + L.lay.field + (size_t)(q) * L.lay.field##_ps)
+#define WS1(T, field) reinterpret_cast<T*>(wb + L.lay.field)
+
+// copy n vertices between (possibly strided) locations, one lane
+__device__ __forceinline__ void copy_fn(Vtx* dst, int dstride, const Vtx* src, int sstride, int n) {
+    for (int i = 0; i < n; ++i) dst[i * dstride] = src[i * sstride];
+}
+
+__device__ __forceinline__ Fn shfl_fn(const Fn& F, int src) {
+    Fn G;
+    G.p = reinterpret_cast<const Vtx*>(__shfl_sync(FULL, reinterpret_cast<unsigned long long>(F.p), src));
+    G.n = __shfl_sync(FULL, F.n, src);
+    G.sl = __shfl_sync(FULL, F.sl, src);
+    G.stride = __shfl_sync(FULL, F.stride, src);
+    return G;
+}
+
+// tier 3: the warp updates every heavy node of this level, one after another
+// (pwl_warp.cuh); results go to the row arena.  Out of line: rare.
+// returns (status bits, this lane's result count, its arena offset)
+__device__ __noinline__ int3 heavy_phase(unsigned hmask, Fn U, Fn D, double lo, double hi, double ux, double uf,
+                                         bool seller, Vtx* hscr, int hcap, Vtx* arena, int* counter, int acap,
+                                         int lane) {
+    int3 res = make_int3(DEV_OK, 0, 0);
+    while (hmask) {
+        const int hl = __ffs(hmask) - 1;
+        hmask &= hmask - 1;
+        const Fn Uh = shfl_fn(U, hl), Dh = shfl_fn(D, hl);
+        const double hlo = __shfl_sync(FULL, lo, hl), hhi = __shfl_sync(FULL, hi, hl);
+        const double hux = __shfl_sync(FULL, ux, hl), huf = __shfl_sync(FULL, uf, hl);
+        int zoff = 0, zn = 0, e;
+        if (22 * (Uh.n + Dh.n) + 2300 > hcap) {
+            e = DEV_OVERFLOW;
+        } else {
+            e = warp_node_update(Uh, Dh, hlo, hhi, hux, huf, seller, hscr, hcap, arena, counter, acap, zoff, zn,
+                                 lane);
+        }
+        if (lane == hl) res = make_int3(e, zn, zoff);
+    }
+    return res;
+}
+
+// a6: root, t = 0, no costs (derived A.4): v_0(y) = min_b [w_0(b) + S0 b] - S0 y
+// over the vertices b of w_0 = max(z_{1,0}, z_{1,1}); returns the status bits.
+__device__ __noinline__ int root_phase(Fn mine, OptionConsts oc, bool seller, Vtx* hscr, int hcap,
+                                       Quote* q, int lane) {
+    const Fn Ur = shfl_fn(mine, 0), Dr = shfl_fn(mine, 1);
+    int nW = 0;
+    double slW = 0.0;
+    const int nE = Ur.n + Dr.n;
+    int e = (6 * nE + 200 > hcap) ? DEV_OVERFLOW
+                                  : warp_merge_max(Ur, Dr, hscr, hscr + 2 * nE + 64, 2 * nE + 2, nW, slW, lane);
+    double mv = INFINITY;
+    if (!e) {
+        const Vtx* Wv = hscr + 2 * nE + 64;
+        for (int i = lane; i < nW; i += 32) mv = fmin(mv, fma(oc.S0, Wv[i].x, Wv[i].f));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mv = fmin(mv, __shfl_xor_sync(FULL, mv, o));
+        if (!(slW + oc.S0 < 0.0) || !(Wv[nW - 1].s + oc.S0 > 0.0)) e = DEV_UNBOUNDED;
+    }
+    if (lane == 0 && !e) {
+        double xi, zeta;
+        option_payoff(oc, oc.S0, xi, zeta);
+        const double intrinsic = xi + zeta * oc.S0;     // u_0(0): S^a_0 = S^b_0 = S0
+        if (seller) q->ask = fmax(intrinsic, mv);       // pi^a = z_0(0)
+        else q->bid = fmax(intrinsic, -mv);             // pi^b = -z'_0(0)
+    }
+    return e;
+}
+
+template <int C, int B, int WARPS, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_constant__ StripLaunch L) {
+    extern __shared__ __align__(16) char smem_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    StripSmem<C, B>& S = reinterpret_cast<StripSmem<C, B>*>(smem_raw)[wib];
+    const int N = L.N;
+    char* const wb = L.ws + (size_t)(blockIdx.x * WARPS + wib) * L.lay.total;
+    double* const Epow = WS1(double, epow);
+    double* const Dpow = WS1(double, dpow);
+
+    for (;;) {
+        int it = 0;
+        if (lane == 0) it = atomicAdd(L.work_counter, 1);
+        it = __shfl_sync(FULL, it, 0);
+        if (it >= *L.n_items) break;
+        const int code = L.items[it];
+        const int64_t opt = code >> 1;
+        const bool seller = (code & 1) == 0;
+        OptionConsts oc;
+        if (validate_option(L.in, opt, N, true, oc) != STATUS_OK) continue;  // status set by prepare
+
+        // a1: per-option tables: S_{t,j} = S0 e^{h (t-2j)}, r^-t = e^{-rho t}
+        for (int i = lane; i < 2 * N + 3; i += 32) Epow[i] = exp(oc.h * (double)(i - (N + 1)));
+        for (int t = lane; t < N + 2; t += 32) Dpow[t] = exp(-oc.rho * (double)t);
+        __syncwarp();
+        const double kp = 1.0 + oc.k, km = 1.0 - oc.k;  // ask / bid factors
+        int err = DEV_OK;
+        int maxn = 1;
+        unsigned long long vsum = 0;
+
+        for (int s = N / SW; s >= 0 && !err; --s) {
+            const int j0 = s * SW, j = j0 + lane;
+            const int cout = s & 1, cin = cout ^ 1;
+            // a2: leaves t = N+1, payoff (0,0): z = y^- S^a - y^+ S^b
+            int my_n = 0, my_off = -1;
+            double my_sl = 0.0;
+            if (j <= N + 1) {
+                const double Sd = oc.S0 * Epow[(N + 1) - 2 * j + (N + 1)] * Dpow[N + 1];
+                Vtx& v = S.row[lane];
+                v.x = 0.0;
+                v.f = 0.0;
+                v.s = -km * Sd;
+                my_n = 1;
+                my_sl = -kp * Sd;
+                if (lane == 31 && j + 1 <= N + 1) {
+                    const double Sd1 = oc.S0 * Epow[(N + 1) - 2 * (j + 1) + (N + 1)] * Dpow[N + 1];
+                    S.leaf31.x = 0.0;
+                    S.leaf31.f = 0.0;
+                    S.leaf31.s = -km * Sd1;
+                }
+            }
+            const double leaf31_sl = -kp * oc.S0 * Epow[max((N + 1) - 2 * (j + 1) + (N + 1), 0)] * Dpow[N + 1];
+            if (lane == 0) {
+                S.rcnt[0] = 0;
+                S.rcnt[1] = 0;
+                S.ccnt = 0;
+            }
+            __syncwarp();
+            int cur = 0;
+            for (int t = N; t >= max(j0, 1); --t) {
+                const int nxt = cur ^ 1;
+                const bool active = j <= t;
+                // children: up = own previous; down = lane+1's previous / carry / leaf
+                const int dn = __shfl_down_sync(FULL, my_n, 1);
+                const int doff = __shfl_down_sync(FULL, my_off, 1);
+                const double dsl = __shfl_down_sync(FULL, my_sl, 1);
+                Vtx* const rcur = WS(Vtx, rarena, cur);
+                const Fn U = (my_off < 0) ? make_fn(&S.row[lane], my_n, my_sl, SW)
+                                          : make_fn(rcur + my_off, my_n, my_sl, 1);
+                Fn D;
+                if (lane < 31) {
+                    D = (doff < 0) ? make_fn(&S.row[lane + 1], dn, dsl, SW) : make_fn(rcur + doff, dn, dsl, 1);
+                } else if (t == N) {
+                    D = make_fn(&S.leaf31, 1, leaf31_sl, 1);  // the analytic leaf (N+1, j+1)
+                } else if (active) {
+                    const int2 h = WS(int2, chdr, cin)[t + 1];
+                    const double csl = WS(double, csl, cin)[t + 1];
+                    D = (h.y < 0) ? make_fn(WS(Vtx, cv, cin) + (size_t)(t + 1) * C, h.x, csl, 1)
+                                  : make_fn(WS(Vtx, carena, cin) + h.y, h.x, csl, 1);
+                } else {
+                    D = make_fn(&S.leaf31, 0, 0.0, 1);
+                }
+                // node constants: quotes (discounted), exercise function u_t (P:96 / P:133)
+                const double S_ = oc.S0 * Epow[max(t - 2 * j + (N + 1), 0)];  // idle lanes: any index
+                const double disc = Dpow[t];
+                const double lo = -kp * S_ * disc, hi = -km * S_ * disc;
+                double xi, zeta;
+                option_payoff(oc, S_, xi, zeta);
+                const double ux = seller ? zeta : -zeta;
+                const double uf = (seller ? xi : -xi) * disc;
+
+                // tier 1 / tier 2: sequential update by this lane (pwl_lane.cuh).
+                // Pass 1 reads the children and leaves A in the lane's scratch
+                // (shared; the lane's global scratch when it outgrows B vertices).
+                Vtx* const lg0 = WS1(Vtx, lscr) + (size_t)lane * 2 * L.caps.BG;
+                int nA = 0;
+                double slA = lo;
+                int where = 0;  // A in: 1 = shared scratch, 2 = lane global scratch
+                bool heavy = false;
+                if (active) {
+                    heavy = U.n + D.n > L.caps.TL;
+                    // attempt 0: shared scratch; attempt 1: the lane's global scratch
+                    for (int attempt = 0; attempt < 2 && !heavy; ++attempt) {
+                        Vtx* const buf = attempt ? lg0 : &S.s0[lane];
+                        const int e = lane_pass1(U, D, lo, buf, attempt ? L.caps.BG : B, attempt ? 1 : SW, nA, slA);
+                        where = attempt + 1;
+                        if (e != DEV_OVERFLOW) {
+                            err |= e;
+                            break;
+                        }
+                        if (attempt) heavy = true;  // too big for a lane: the warp takes it
+                    }
+                    if (heavy) where = 0;
+                }
+                // tier 3: warp-cooperative updates of this level's heavy nodes
+                const unsigned hmask = __ballot_sync(FULL, heavy);
+                int h_n = 0, h_off = 0;
+                if (hmask) {
+                    const int3 hr = heavy_phase(hmask, U, D, lo, hi, ux, uf, seller, WS1(Vtx, hscr), L.caps.hscr_cap,
+                                                WS(Vtx, rarena, nxt), &S.rcnt[nxt], L.caps.rarena_cap, lane);
+                    err |= hr.x;
+                    h_n = hr.y;
+                    h_off = hr.z;
+                }
+                __syncwarp();
+                // pass 2 writes Z over the previous row, which is dead now (every
+                // lane has read its children)
+                if (active) {
+                    if (heavy) {
+                        my_n = h_n;
+                        my_off = h_off;
+                        my_sl = lo;
+                    } else if (where && !err) {
+                        const Fn A = (where == 1) ? make_fn(&S.s0[lane] + (size_t)(B - nA) * SW, nA, slA, SW)
+                                                  : make_fn(lg0 + (L.caps.BG - nA), nA, slA, 1);
+                        Vtx* const lg1 = lg0 + L.caps.BG;
+                        Emit E;
+                        int e = DEV_OK;
+                        // attempt 0: straight into the row slot; 1: more than C vertices,
+                        // via the lane scratch into the row arena
+                        for (int attempt = 0; attempt < 2; ++attempt) {
+                            E.out = attempt ? lg1 : &S.row[lane];
+                            E.cap = attempt ? L.caps.BG : C;
+                            E.stride = attempt ? 1 : SW;
+                            e = lane_pass2(A, lo, hi, ux, uf, seller, E);
+                            if (e != DEV_OVERFLOW) break;
+                        }
+                        my_off = -1;
+                        if (!e && E.out == lg1) {
+                            const int off = atomicAdd(&S.rcnt[nxt], E.m);
+                            if (off + E.m > L.caps.rarena_cap) {
+                                e = DEV_OVERFLOW;
+                            } else {
+                                copy_fn(WS(Vtx, rarena, nxt) + off, 1, lg1, 1, E.m);
+                                my_off = off;
+                            }
+                        }
+                        err |= e;
+                        my_n = E.m;
+                        my_sl = E.sl;
+                    }
+                    vsum += (unsigned long long)my_n;
+                    maxn = max(maxn, my_n);
+                }
+                __syncwarp();
+                // carry out: node (t, j0), read by the strip to the left (its lane 31 at level t-1)
+                {
+                    const int c_n = __shfl_sync(FULL, my_n, 0);
+                    const int c_off = __shfl_sync(FULL, my_off, 0);
+                    if (lane == 0) WS(double, csl, cout)[t] = my_sl;
+                    if (c_off < 0) {
+                        if (lane < c_n) WS(Vtx, cv, cout)[(size_t)t * C + lane] = S.row[lane * SW];
+                        if (lane == 0) WS(int2, chdr, cout)[t] = make_int2(c_n, -1);
+                    } else {
+                        int base = 0;
+                        if (lane == 0) base = atomicAdd(&S.ccnt, c_n);
+                        base = __shfl_sync(FULL, base, 0);
+                        if (base + c_n > L.caps.carena_cap) {
+                            err |= DEV_OVERFLOW;
+                        } else {
+                            Vtx* const ca = WS(Vtx, carena, cout) + base;
+                            const Vtx* const ra = WS(Vtx, rarena, nxt) + c_off;
+                            for (int i = lane; i < c_n; i += 32) ca[i] = ra[i];
+                            if (lane == 0) WS(int2, chdr, cout)[t] = make_int2(c_n, base);
+                        }
+                    }
+                }
+                if (lane == 0) S.rcnt[cur] = 0;  // level t+1's arena is dead
+                cur = nxt;
+                err = __reduce_or_sync(FULL, err);
+                if (err) break;
+                __syncwarp();
+            }
+            __syncwarp();
+            if (s == 0 && !err) {
+                const Fn mine = (my_off < 0) ? make_fn(&S.row[lane], my_n, my_sl, SW)
+                                             : make_fn(WS(Vtx, rarena, cur) + my_off, my_n, my_sl, 1);
+                err |= root_phase(mine, oc, seller, WS1(Vtx, hscr), L.caps.hscr_cap, &L.out[opt], lane);
+            }
+        }
+        // per-item bookkeeping
+        err = __reduce_or_sync(FULL, err);
+        maxn = __reduce_max_sync(FULL, maxn);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) vsum += __shfl_xor_sync(FULL, vsum, o);
+        if (lane == 0) {
+            atomicAdd(L.vertex_sum, vsum);
+            if (err & DEV_OVERFLOW) {
+                const int q = atomicAdd(L.ovf_count, 1);
+                L.ovf_items[q] = code;
+            } else if (err & DEV_UNBOUNDED) {
+                atomicMax(&L.out[opt].status, STATUS_EUNBOUNDED);
+            }
+            atomicMax(&L.out[opt].max_bp, maxn);
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+constexpr int STRIP_C = 6, STRIP_B = 8, STRIP_WARPS = 4, STRIP_MINB = 4;
+#define STRIP_KERNEL strip_kernel<STRIP_C, STRIP_B, STRIP_WARPS, STRIP_MINB>
+constexpr size_t STRIP_SMEM = sizeof(StripSmem<STRIP_C, STRIP_B>) * STRIP_WARPS;
+
+static int strip_set_smem() {
+    static int done = 0;
+    if (!done) {
+        if (cudaFuncSetAttribute(STRIP_KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)STRIP_SMEM) !=
+            cudaSuccess)
+            return STATUS_ECUDA;
+        done = 1;
+    }
+    return STATUS_OK;
+}
+
+StripCaps strip_caps(int N, int level) {
+    // level 0: first pass; each retry level quadruples the arenas
+    StripCaps c;
+    c.C = STRIP_C;
+    c.B = STRIP_B;
+    c.BG = 256;
+    c.TL = 64;
+    const int64_t mul = (int64_t)1 << (2 * level);
+    auto clampi = [](int64_t v) { return (int)(v > ((int64_t)1 << 28) ? ((int64_t)1 << 28) : v); };
+    c.rarena_cap = clampi(mul * (16 * (int64_t)(N + 2) + 4096));
+    c.carena_cap = clampi(mul * (16 * (int64_t)(N + 2) + 4096));
+    c.hscr_cap = clampi(mul * (22 * 8 * (int64_t)(N + 2) + 2300 + 4096));
+    return c;
+}
+
+size_t strip_ws_bytes_per_warp(int N, int level) { return strip_layout(N, strip_caps(N, level)).total; }
+
+int strip_warps_per_cta() { return STRIP_WARPS; }
+
+int strip_ctas_per_sm() {
+    int b = 0;
+    if (strip_set_smem() != STATUS_OK) return 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, STRIP_KERNEL, STRIP_WARPS * 32, STRIP_SMEM);
+    return b;
+}
+
+int strip_launch(const StripLaunchArgs& a, cudaStream_t s) {
+    StripLaunch L;
+    L.in = a.in;
+    L.N = a.N;
+    L.out = a.out;
+    L.items = a.items;
+    L.n_items = a.n_items;
+    L.work_counter = a.work_counter;
+    L.ovf_items = a.ovf_items;
+    L.ovf_count = a.ovf_count;
+    L.vertex_sum = a.vertex_sum;
+    L.ws = a.ws;
+    L.caps = strip_caps(a.N, a.level);
+    L.lay = strip_layout(a.N, L.caps);
+    if (L.lay.total != a.ws_stride) return STATUS_EINVAL;
+    if (strip_set_smem() != STATUS_OK) return STATUS_ECUDA;
+    STRIP_KERNEL<<<a.ctas, STRIP_WARPS * 32, STRIP_SMEM, s>>>(L);
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? STATUS_OK : STATUS_ECUDA;
+}
+
+}  // namespace amtc

@@ -56,7 +56,7 @@ __device__ __forceinline__ int merge_split(const Fn& U, const Fn& D, int k) {
     int lo = max(0, k - D.n), hi = min(k, U.n);
     while (lo < hi) {
         int mid = (lo + hi) >> 1;
-        if (U.v[mid].x <= D.v[k - mid - 1].x) lo = mid + 1;
+        if (U.v(mid).x <= D.v(k - mid - 1).x) lo = mid + 1;
         else hi = mid;
     }
     return lo;
@@ -82,16 +82,16 @@ __device__ __forceinline__ int warp_merge_max(const Fn& F, const Fn& G, Vtx* raw
     bool curF;
     double xprev, eF, eG;
     {
-        double xe0 = fmin(F.v[0].x, G.v[0].x);
+        double xe0 = fmin(F.v(0).x, G.v(0).x);
         double eF0 = piece_at(F, -1, xe0), eG0 = piece_at(G, -1, xe0);
         if (F.sl != G.sl) curF = F.sl < G.sl;
         else curF = eF0 >= eG0;
         slW = curF ? F.sl : G.sl;
     }
     if (k0 > 0) {
-        xprev = fmax(iF >= 0 ? F.v[iF].x : -INFINITY, iG >= 0 ? G.v[iG].x : -INFINITY);
-        eF = (iF >= 0 && F.v[iF].x == xprev) ? F.v[iF].f : piece_at(F, iF, xprev);
-        eG = (iG >= 0 && G.v[iG].x == xprev) ? G.v[iG].f : piece_at(G, iG, xprev);
+        xprev = fmax(iF >= 0 ? F.v(iF).x : -INFINITY, iG >= 0 ? G.v(iG).x : -INFINITY);
+        eF = (iF >= 0 && F.v(iF).x == xprev) ? F.v(iF).f : piece_at(F, iF, xprev);
+        eG = (iG >= 0 && G.v(iG).x == xprev) ? G.v(iG).f : piece_at(G, iG, xprev);
         if (fabs(eF - eG) > ftol(eF, eG)) curF = eF > eG;
         else curF = sF >= sG;
     } else {
@@ -103,13 +103,13 @@ __device__ __forceinline__ int warp_merge_max(const Fn& F, const Fn& G, Vtx* raw
     E.init(mine, 2 * (k1 - k0) + 2, curF ? sF : sG);
     double xe = xprev;
     for (int k = k0; k < k1; ++k) {
-        double xF = (iF + 1 < F.n) ? F.v[iF + 1].x : INFINITY;
-        double xG = (iG + 1 < G.n) ? G.v[iG + 1].x : INFINITY;
+        double xF = (iF + 1 < F.n) ? F.v(iF + 1).x : INFINITY;
+        double xG = (iG + 1 < G.n) ? G.v(iG + 1).x : INFINITY;
         // merged order takes F first on ties: exactly one vertex per event
         const bool takeF = xF <= xG;
         xe = takeF ? xF : xG;
-        eF = (takeF) ? F.v[iF + 1].f : piece_at(F, iF, xe);
-        eG = (!takeF) ? G.v[iG + 1].f : piece_at(G, iG, xe);
+        eF = (takeF) ? F.v(iF + 1).f : piece_at(F, iF, xe);
+        eG = (!takeF) ? G.v(iG + 1).f : piece_at(G, iG, xe);
         const double tl = ftol(eF, eG);
         bool lost = curF ? (eG > eF + tl) : (eF > eG + tl);
         if (lost) {
@@ -119,8 +119,8 @@ __device__ __forceinline__ int warp_merge_max(const Fn& F, const Fn& G, Vtx* raw
             double fc = curF ? piece_at(F, iF, yc) : piece_at(G, iG, yc);
             E.push(yc, fc, curF ? sF : sG);
         }
-        if (takeF) { iF++; sF = F.v[iF].s; }
-        else { iG++; sG = G.v[iG].s; }
+        if (takeF) { iF++; sF = F.v(iF).s; }
+        else { iG++; sG = G.v(iG).s; }
         if (fabs(eF - eG) > tl) curF = eF > eG;
         else curF = sF >= sG;
         E.push(xe, fmax(eF, eG), curF ? sF : sG);
@@ -143,8 +143,8 @@ __device__ __forceinline__ int warp_merge_max(const Fn& F, const Fn& G, Vtx* raw
     __syncwarp();
     copy_vtx(W + off, mine, E.m);
     if (total == 0 && lane == 0) {  // both children are one line: anchor
-        W[0].x = F.v[0].x;
-        W[0].f = fmax(F.v[0].f, piece_at(G, -1, F.v[0].x));
+        W[0].x = F.v(0).x;
+        W[0].f = fmax(F.v(0).f, piece_at(G, -1, F.v(0).x));
         W[0].s = slW;
     }
     nW = total == 0 ? 1 : total;

@@ -35,7 +35,8 @@ int main(int argc, char** argv) {
                 double xi, zeta;
                 if (kind == 0) { xi = K; zeta = -1; } else if (kind == 1) { xi = -K; zeta = 1; }
                 else { xi = fmax(S - K, 0.0) - fmax(S - K2, 0.0); zeta = 0; }
-                Fn U{z[j].data(), (int)z[j].size(), sl[j]}, D{z[j + 1].data(), (int)z[j + 1].size(), sl[j + 1]};
+                const Fn U = make_fn(z[j].data(), (int)z[j].size(), sl[j]);
+                const Fn D = make_fn(z[j + 1].data(), (int)z[j + 1].size(), sl[j + 1]);
                 int b = 4 * (U.n + D.n) + 16;
                 std::vector<Vtx> r0(b), r1(b);
                 int nZ; double slZ;
@@ -62,7 +63,8 @@ int main(int argc, char** argv) {
         }
         // root
         std::vector<Vtx> w(4 * (z[0].size() + z[1].size()) + 16);
-        Fn U{z[0].data(), (int)z[0].size(), sl[0]}, D{z[1].data(), (int)z[1].size(), sl[1]};
+        const Fn U = make_fn(z[0].data(), (int)z[0].size(), sl[0]);
+        const Fn D = make_fn(z[1].data(), (int)z[1].size(), sl[1]);
         Emit E; E.out = w.data(); E.cap = (int)w.size();
         envelope(U, D, true, E);
         double mv = INFINITY;
