@@ -141,6 +141,12 @@ typedef struct {
 } amtc_tc_stats;
 int amtc_tc_last_stats(amtc_tc_stats* out);
 
+/* TESTING HOOK (not for production use): node updates whose two children hold
+   more than `tl` vertices in total take the warp-cooperative path (default 64);
+   a small tl forces that path onto ordinary nodes so tests can check it
+   against the oracle.  tl <= 0 restores the default.  Affects later calls. */
+void amtc_debug_set_heavy_threshold(int tl);
+
 #ifdef __cplusplus
 }
 #endif

@@ -48,7 +48,7 @@ assert QUOTE_DTYPE.itemsize == C.sizeof(Quote) == 24
 
 EXPORTS = ["amtc_price_american_tc", "amtc_price_american_tc_batch", "amtc_price_american_tc_batch_host",
            "amtc_price_crr_batch", "amtc_price_crr_batch_host", "amtc_strerror", "amtc_last_error",
-           "amtc_launch_count", "amtc_tc_last_stats"]
+           "amtc_launch_count", "amtc_tc_last_stats", "amtc_debug_set_heavy_threshold"]
 
 _lib = None
 
@@ -76,6 +76,8 @@ def lib():
         L.amtc_launch_count.restype = C.c_int64
         L.amtc_tc_last_stats.restype = C.c_int
         L.amtc_tc_last_stats.argtypes = [C.POINTER(TcStats)]
+        L.amtc_debug_set_heavy_threshold.restype = None
+        L.amtc_debug_set_heavy_threshold.argtypes = [C.c_int]
         _lib = L
     return _lib
 
@@ -93,6 +95,12 @@ def strerror(status: int) -> str:
 
 def launch_count() -> int:
     return int(lib().amtc_launch_count())
+
+
+def debug_set_heavy_threshold(tl: int) -> None:
+    """Testing hook: route node updates whose children hold > tl vertices to the
+    warp-cooperative path (tl <= 0: default)."""
+    lib().amtc_debug_set_heavy_threshold(int(tl))
 
 
 def tc_last_stats() -> dict:

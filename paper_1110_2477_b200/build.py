@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libamtc.so")
 SOURCES = ["amtc_capi.cu", "amtc_prepare.cu", "amtc_strip.cu", "amtc_crr.cu"]
-HEADERS = ["amtc_internal.cuh", "amtc_option.cuh", "pwl_device.cuh", "pwl_warp.cuh"]
+HEADERS = ["amtc_internal.cuh", "amtc_option.cuh", "pwl_device.cuh", "pwl_lane.cuh", "pwl_heavy.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr",

@@ -338,6 +338,8 @@ const char* amtc_strerror(int status) {
 
 const char* amtc_last_error(void) { return g_last_error.c_str(); }
 
+void amtc_debug_set_heavy_threshold(int tl) { strip_set_heavy_threshold(tl); }
+
 int64_t amtc_launch_count(void) { return g_launches.load(); }
 
 int amtc_tc_last_stats(amtc_tc_stats* out) {

@@ -67,6 +67,7 @@ size_t strip_ws_bytes_per_warp(int N, int level);
 int strip_warps_per_cta();
 int strip_ctas_per_sm();
 int strip_launch(const StripLaunchArgs& a, cudaStream_t s);
+void strip_set_heavy_threshold(int tl);
 
 // amtc_crr.cu
 int crr_launch(const BatchPtrs& in, int64_t n, int N, double* out, cudaStream_t s);

@@ -31,7 +31,7 @@
 //   * node-update scratch: B vertices x 2 buffers per lane in shared memory;
 //     a node that outgrows it re-runs with per-lane global scratch (tier 2);
 //   * nodes whose children hold more than TL vertices in total are updated by
-//     the whole warp cooperatively (pwl_warp.cuh, tier 3).
+//     the whole warp cooperatively (pwl_heavy.cuh, tier 3).
 // Any capacity overflow aborts the item; the host re-runs it with larger
 // arenas (amtc_capi.cu), never truncating a function.
 #include <cuda_runtime.h>
@@ -39,8 +39,8 @@
 #include "amtc_internal.cuh"
 #include "amtc_option.cuh"
 #include "pwl_device.cuh"
+#include "pwl_heavy.cuh"
 #include "pwl_lane.cuh"
-#include "pwl_warp.cuh"
 
 namespace amtc {
 
@@ -121,6 +121,9 @@ __device__ __forceinline__ void copy_fn(Vtx* dst, int dstride, const Vtx* src, i
     for (int i = 0; i < n; ++i) dst[i * dstride] = src[i * sstride];
 }
 
+
+constexpr unsigned FULL = 0xffffffffu;
+
 __device__ __forceinline__ Fn shfl_fn(const Fn& F, int src) {
     Fn G;
     G.p = reinterpret_cast<const Vtx*>(__shfl_sync(FULL, reinterpret_cast<unsigned long long>(F.p), src));
@@ -131,8 +134,8 @@ __device__ __forceinline__ Fn shfl_fn(const Fn& F, int src) {
 }
 
 // tier 3: the warp updates every heavy node of this level, one after another
-// (pwl_warp.cuh); results go to the row arena.  Out of line: rare.
-// returns (status bits, this lane's result count, its arena offset)
+// (pwl_heavy.cuh); results go to the row arena.  Out of line: rare.
+// Returns (status bits, this lane's result count, its arena offset).
 __device__ __noinline__ int3 heavy_phase(unsigned hmask, Fn U, Fn D, double lo, double hi, double ux, double uf,
                                          bool seller, Vtx* hscr, int hcap, Vtx* arena, int* counter, int acap,
                                          int lane) {
@@ -143,13 +146,9 @@ __device__ __noinline__ int3 heavy_phase(unsigned hmask, Fn U, Fn D, double lo, 
         const Fn Uh = shfl_fn(U, hl), Dh = shfl_fn(D, hl);
         const double hlo = __shfl_sync(FULL, lo, hl), hhi = __shfl_sync(FULL, hi, hl);
         const double hux = __shfl_sync(FULL, ux, hl), huf = __shfl_sync(FULL, uf, hl);
-        int zoff = 0, zn = 0, e;
-        if (22 * (Uh.n + Dh.n) + 2300 > hcap) {
-            e = DEV_OVERFLOW;
-        } else {
-            e = warp_node_update(Uh, Dh, hlo, hhi, hux, huf, seller, hscr, hcap, arena, counter, acap, zoff, zn,
-                                 lane);
-        }
+        int zoff = 0, zn = 0;
+        const int e = heavy::node_update(Uh, Dh, hlo, hhi, hux, huf, seller, hscr, hcap, arena, counter, acap, zoff,
+                                         zn, lane);
         if (lane == hl) res = make_int3(e, zn, zoff);
     }
     return res;
@@ -157,30 +156,20 @@ __device__ __noinline__ int3 heavy_phase(unsigned hmask, Fn U, Fn D, double lo, 
 
 // a6: root, t = 0, no costs (derived A.4): v_0(y) = min_b [w_0(b) + S0 b] - S0 y
 // over the vertices b of w_0 = max(z_{1,0}, z_{1,1}); returns the status bits.
-__device__ __noinline__ int root_phase(Fn mine, OptionConsts oc, bool seller, Vtx* hscr, int hcap,
-                                       Quote* q, int lane) {
+__device__ __noinline__ int root_phase(Fn mine, OptionConsts oc, bool seller, Quote* q, int lane) {
     const Fn Ur = shfl_fn(mine, 0), Dr = shfl_fn(mine, 1);
-    int nW = 0;
-    double slW = 0.0;
-    const int nE = Ur.n + Dr.n;
-    int e = (6 * nE + 200 > hcap) ? DEV_OVERFLOW
-                                  : warp_merge_max(Ur, Dr, hscr, hscr + 2 * nE + 64, 2 * nE + 2, nW, slW, lane);
-    double mv = INFINITY;
-    if (!e) {
-        const Vtx* Wv = hscr + 2 * nE + 64;
-        for (int i = lane; i < nW; i += 32) mv = fmin(mv, fma(oc.S0, Wv[i].x, Wv[i].f));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mv = fmin(mv, __shfl_xor_sync(FULL, mv, o));
-        if (!(slW + oc.S0 < 0.0) || !(Wv[nW - 1].s + oc.S0 > 0.0)) e = DEV_UNBOUNDED;
-    }
-    if (lane == 0 && !e) {
+    double slW, srW;
+    const double mv = heavy::root_min(Ur, Dr, oc.S0, slW, srW, lane);
+    // the minimum exists iff w_0 + S0 y has a decreasing left and increasing right tail
+    if (!(slW + oc.S0 < 0.0) || !(srW + oc.S0 > 0.0)) return DEV_UNBOUNDED;
+    if (lane == 0) {
         double xi, zeta;
         option_payoff(oc, oc.S0, xi, zeta);
-        const double intrinsic = xi + zeta * oc.S0;     // u_0(0): S^a_0 = S^b_0 = S0
-        if (seller) q->ask = fmax(intrinsic, mv);       // pi^a = z_0(0)
-        else q->bid = fmax(intrinsic, -mv);             // pi^b = -z'_0(0)
+        const double intrinsic = xi + zeta * oc.S0;  // u_0(0): S^a_0 = S^b_0 = S0
+        if (seller) q->ask = fmax(intrinsic, mv);    // pi^a = z_0(0)
+        else q->bid = fmax(intrinsic, -mv);          // pi^b = -z'_0(0)
     }
-    return e;
+    return DEV_OK;
 }
 
 template <int C, int B, int WARPS, int MINB>
@@ -380,7 +369,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
             if (s == 0 && !err) {
                 const Fn mine = (my_off < 0) ? make_fn(&S.row[lane], my_n, my_sl, SW)
                                              : make_fn(WS(Vtx, rarena, cur) + my_off, my_n, my_sl, 1);
-                err |= root_phase(mine, oc, seller, WS1(Vtx, hscr), L.caps.hscr_cap, &L.out[opt], lane);
+                err |= root_phase(mine, oc, seller, &L.out[opt], lane);
             }
         }
         // per-item bookkeeping
@@ -420,18 +409,21 @@ static int strip_set_smem() {
     return STATUS_OK;
 }
 
+static int g_tl_override = 0;  // testing hook (amtc_debug_set_heavy_threshold)
+void strip_set_heavy_threshold(int tl) { g_tl_override = tl > 0 ? tl : 0; }
+
 StripCaps strip_caps(int N, int level) {
     // level 0: first pass; each retry level quadruples the arenas
     StripCaps c;
     c.C = STRIP_C;
     c.B = STRIP_B;
     c.BG = 256;
-    c.TL = 64;
+    c.TL = g_tl_override ? g_tl_override : 64;
     const int64_t mul = (int64_t)1 << (2 * level);
     auto clampi = [](int64_t v) { return (int)(v > ((int64_t)1 << 28) ? ((int64_t)1 << 28) : v); };
-    c.rarena_cap = clampi(mul * (16 * (int64_t)(N + 2) + 4096));
-    c.carena_cap = clampi(mul * (16 * (int64_t)(N + 2) + 4096));
-    c.hscr_cap = clampi(mul * (22 * 8 * (int64_t)(N + 2) + 2300 + 4096));
+    c.rarena_cap = clampi(mul * (32 * (int64_t)(N + 2) + 4096));
+    c.carena_cap = clampi(mul * (32 * (int64_t)(N + 2) + 4096));
+    c.hscr_cap = clampi(heavy::STAGE * 32 + mul * (2 * (int64_t)(N + 2) + 4096));
     return c;
 }
 

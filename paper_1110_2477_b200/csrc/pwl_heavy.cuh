@@ -1,0 +1,888 @@
+// pwl_heavy.cuh -- warp-cooperative node update for HEAVY node functions (the
+// buyer's "sawtooth" of calls / bull spreads: thousands of vertices, DESIGN.md
+// "Breakpoint counts").  Chunk-synchronous: the merged vertex sequence of the
+// two children is cut into blocks of 32 events and lane i owns event 32 b + i,
+// so loads are coalesced and all lanes do the same work.
+//
+// Data-parallel form of one node (Sec. 3; reading A7): with
+//   W = max(U, D)                              (discounted, so no /r)
+//   g_j = W_j - lo x_j,  h_j = W_j - hi x_j    over the vertices x_j of W,
+//   M_j = min_{i >= j} g_i,  P_j = min_{i <= j} h_i,
+// the restriction of W to slopes [lo, hi] is, on the piece (x_j, x_{j+1}),
+//   v(y) = min( W(y), lo y + M_{j+1}, hi y + P_j )
+// (the infimum of a piecewise-linear function over a half line is attained at
+// its end point or at a vertex; the tails are monotone when d < r < u), and
+// z = max(u, v) (seller) / min(u, v) (buyer).
+// Sweep 1 (right to left) stores, per block, the suffix minimum of g and the
+// first vertex of W to its right; sweep 2 (left to right) rebuilds W, scans M
+// and P inside the block, and the lane owning W vertex j emits z's vertices on
+// [x_j, x_{j+1}).  Vertices are staged per lane, de-duplicated against the
+// slope arriving from the left, and compacted with a warp prefix sum.
+#pragma once
+#include "pwl_device.cuh"
+
+namespace amtc {
+namespace heavy {
+
+constexpr unsigned FULLM = 0xffffffffu;
+constexpr int STAGE = 40;  // staged output vertices per lane per block
+
+// merged event k: the k-th vertex of U and D by x (U first on ties)
+struct Ev {
+    double x, eU, eD, sUL, sUR, sDL, sDR;
+    bool skip;  // a D vertex at the x of the previous (U) event, which handled both
+};
+
+// number of U events among the first k (merge path), searched in [lo, hi]
+__device__ __forceinline__ int split(const Fn& U, const Fn& D, int k, int lo, int hi) {
+    lo = max(lo, k - D.n);
+    hi = min(hi, min(k, U.n));
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (U.v(mid).x <= D.v(k - mid - 1).x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ Ev event_at(const Fn& U, const Fn& D, int k, int a) {
+    Ev e;
+    e.skip = false;
+    const int b = k - a;
+    const bool isU = a < U.n && (b >= D.n || U.v(a).x <= D.v(b).x);
+    if (isU) {
+        const Vtx u = U.v(a);
+        e.x = u.x; e.eU = u.f; e.sUR = u.s; e.sUL = a > 0 ? U.v(a - 1).s : U.sl;
+        if (b < D.n && D.v(b).x == e.x) {  // coincident vertices: one event
+            const Vtx d = D.v(b);
+            e.eD = d.f; e.sDR = d.s; e.sDL = b > 0 ? D.v(b - 1).s : D.sl;
+        } else {
+            const int p = b - 1;
+            const Vtx d = D.v(p < 0 ? 0 : p);
+            const double s = p < 0 ? D.sl : d.s;
+            e.eD = fma(s, e.x - d.x, d.f); e.sDL = s; e.sDR = s;
+        }
+    } else {
+        const Vtx d = D.v(b);
+        e.x = d.x; e.eD = d.f; e.sDR = d.s; e.sDL = b > 0 ? D.v(b - 1).s : D.sl;
+        if (a > 0 && U.v(a - 1).x == e.x) {
+            e.skip = true;
+            const Vtx u = U.v(a - 1);
+            e.eU = u.f; e.sUR = u.s; e.sUL = a > 1 ? U.v(a - 2).s : U.sl;
+        } else {
+            const int p = a - 1;
+            const Vtx u = U.v(p < 0 ? 0 : p);
+            const double s = p < 0 ? U.sl : u.s;
+            e.eU = fma(s, e.x - u.x, u.f); e.sUL = s; e.sUR = s;
+        }
+    }
+    return e;
+}
+
+// winner of max(U, D) just right / just left of the event (ties: by slope)
+__device__ __forceinline__ bool winR(const Ev& e) {
+    const double tl = ftol(e.eU, e.eD);
+    return fabs(e.eU - e.eD) > tl ? e.eU > e.eD : e.sUR >= e.sDR;
+}
+__device__ __forceinline__ bool winL(const Ev& e) {
+    const double tl = ftol(e.eU, e.eD);
+    return fabs(e.eU - e.eD) > tl ? e.eU > e.eD : e.sUL <= e.sDL;
+}
+
+// one vertex of W: position, value, slopes left / right
+struct WV {
+    double x, f, sL, sR;
+};
+
+// the (up to 3) vertices of W owned by one event, in x order
+struct WV3 {
+    WV v0, v1, v2;
+    int n;
+    __device__ __forceinline__ WV get(int q) const { return q == 0 ? v0 : (q == 1 ? v1 : v2); }
+};
+
+// W's vertices produced by event e: a crossing on (x_prev, x), the vertex at
+// x, and (last event only) a crossing on the right tail.  wRp: winner just
+// right of the previous event (for the first event: the left-tail winner);
+// wInf: the right-tail winner.
+__device__ __forceinline__ WV3 w_vertices(const Ev& e, bool valid, double x_prev, bool wRp, bool last,
+                                          bool wInf) {
+    WV3 r;
+    r.n = 0;
+    if (!valid || e.skip) return r;
+    const bool wl = winL(e), wr = winR(e);
+    WV c0, c1, c2;
+    bool h0 = false, h1 = false, h2 = false;
+    if (wRp != wl) {  // crossing on (x_prev, x)
+        const double e_w = wl ? e.eU : e.eD, e_o = wl ? e.eD : e.eU;
+        const double s_w = wl ? e.sUL : e.sDL, s_o = wl ? e.sDL : e.sUL;
+        if (s_w != s_o) {
+            const double y = e.x - (e_w - e_o) / (s_w - s_o);
+            if (y > x_prev && y < e.x) {
+                c0 = WV{y, fma(s_w, y - e.x, e_w), s_o, s_w};
+                h0 = true;
+            }
+        }
+    }
+    const double sWL = wl ? e.sUL : e.sDL, sWR = wr ? e.sUR : e.sDR;
+    if (sWL != sWR) {
+        c1 = WV{e.x, fmax(e.eU, e.eD), sWL, sWR};
+        h1 = true;
+    }
+    if (last && wr != wInf) {  // crossing on (x, +inf)
+        const double e_w = wr ? e.eU : e.eD, e_o = wr ? e.eD : e.eU;
+        const double s_w = wr ? e.sUR : e.sDR, s_o = wr ? e.sDR : e.sUR;
+        if (s_o != s_w) {
+            const double y = e.x + (e_w - e_o) / (s_o - s_w);
+            if (y > e.x) {
+                c2 = WV{y, fma(s_w, y - e.x, e_w), s_w, s_o};
+                h2 = true;
+            }
+        }
+    }
+    r.v0 = h0 ? c0 : (h1 ? c1 : c2);
+    r.v1 = (h0 && h1) ? c1 : c2;
+    r.v2 = c2;
+    r.n = (int)h0 + (int)h1 + (int)h2;
+    return r;
+}
+
+// W vertices of the 32 events of block `blk` (lane i: event 32 blk + i)
+struct BlockW {
+    WV3 w;
+    bool valid;
+};
+
+struct HCtx {
+    Fn U, D;
+    int nE;
+    int klast;     // the last event that is not a skip (it owns the right-tail crossing)
+    bool tailL_U;  // winner at -inf is U
+    bool wInf_U;   // winner at +inf is U
+};
+
+__device__ __forceinline__ HCtx make_ctx(const Fn& U, const Fn& D) {
+    HCtx h;
+    h.U = U;
+    h.D = D;
+    h.nE = U.n + D.n;
+    // coincident last vertices: the last event (D's) is a skip handled by U's
+    h.klast = (U.v(U.n - 1).x == D.v(D.n - 1).x) ? h.nE - 2 : h.nE - 1;
+    const double sUr = U.v(U.n - 1).s, sDr = D.v(D.n - 1).s;
+    // ties (parallel tails): decided by the value far out, i.e. at the outermost vertex
+    if (U.sl != D.sl) h.tailL_U = U.sl < D.sl;
+    else {
+        const double x0 = fmin(U.v(0).x, D.v(0).x);
+        h.tailL_U = piece_at(U, -1, x0) >= piece_at(D, -1, x0);
+    }
+    if (sUr != sDr) h.wInf_U = sUr > sDr;
+    else {
+        const double x1 = fmax(U.v(U.n - 1).x, D.v(D.n - 1).x);
+        h.wInf_U = piece_at(U, U.n - 1, x1) >= piece_at(D, D.n - 1, x1);
+    }
+    return h;
+}
+
+__device__ __forceinline__ BlockW block_w(const HCtx& h, int blk, int lane) {
+    const int k0 = blk * 32;
+    const int a0 = split(h.U, h.D, k0, 0, h.U.n);
+    const int k = k0 + lane;
+    BlockW B;
+    B.valid = k < h.nE;
+    const int kk = B.valid ? k : h.nE - 1;
+    const int a = split(h.U, h.D, kk, a0, a0 + lane);
+    const Ev e = event_at(h.U, h.D, kk, a);
+    const bool wr = winR(e);
+    double x_prev = __shfl_up_sync(FULLM, e.x, 1);
+    bool wRp = __shfl_up_sync(FULLM, (int)wr, 1) != 0;
+    if (lane == 0) {
+        if (k0 == 0) {
+            x_prev = -INFINITY;
+            wRp = h.tailL_U;
+        } else {
+            const int ap = split(h.U, h.D, k0 - 1, max(a0 - 1, 0), a0);
+            const Ev ep = event_at(h.U, h.D, k0 - 1, ap);
+            x_prev = ep.x;
+            wRp = winR(ep);
+        }
+    }
+    B.w = w_vertices(e, B.valid, x_prev, wRp, k == h.klast, h.wInf_U);
+    return B;
+}
+
+// ---------------------------------------------------------------------------
+// z = OP(u, v) on a piece, v = min(W line, lo y + M, hi y + P)
+// ---------------------------------------------------------------------------
+struct Line {
+    double x0, f0, s;
+    __device__ __forceinline__ double at(double y) const { return fma(s, y - x0, f0); }
+};
+
+struct PCtx {
+    double lo, hi, ux, uf;
+    bool seller;
+};
+
+// z's state just right (right = true) or just left of the finite position y:
+// returns z's slope; vi = active v line (0 W, 1 M, 2 P), zU = u wins, zval = z(y)
+__device__ __forceinline__ double z_side(const Line& LW, const Line& LM, bool hasM, const Line& LP, bool hasP,
+                                         const PCtx& c, double y, bool right, int& vi, bool& zU, double& zval) {
+    vi = 0;
+    double vv = LW.at(y), vs = LW.s;
+    if (hasM) {
+        const double m = LM.at(y);
+        const double tl = ftol(m, vv);
+        if (m < vv - tl || (fabs(m - vv) <= tl && (right ? LM.s < vs : LM.s > vs))) { vi = 1; vv = m; vs = LM.s; }
+    }
+    if (hasP) {
+        const double p = LP.at(y);
+        const double tl = ftol(p, vv);
+        if (p < vv - tl || (fabs(p - vv) <= tl && (right ? LP.s < vs : LP.s > vs))) { vi = 2; vv = p; vs = LP.s; }
+    }
+    const double us = (right ? (y >= c.ux) : (y > c.ux)) ? c.hi : c.lo;
+    const double uv = fma(us, y - c.ux, c.uf);
+    const double tl = ftol(uv, vv);
+    bool uw;
+    if (fabs(uv - vv) > tl) uw = c.seller ? (uv > vv) : (uv < vv);
+    else uw = c.seller ? (right ? us > vs : us < vs) : (right ? us < vs : us > vs);
+    zU = uw;
+    zval = c.seller ? fmax(uv, vv) : fmin(uv, vv);
+    return uw ? us : vs;
+}
+
+// where line A meets line B, from values at the finite reference point ref
+__device__ __forceinline__ double cross_at(const Line& A, const Line& B, double ref) {
+    return ref - (A.at(ref) - B.at(ref)) / (A.s - B.s);
+}
+
+// per-lane staging of output vertices (global scratch, lane-interleaved)
+struct Stage {
+    Vtx* buf;  // STAGE x 32
+    int lane, m, err;
+    double last_s;  // slope after the last staged vertex
+    __device__ __forceinline__ void push(double x, double f, double s) {
+        if (m > 0) {
+            Vtx& p = buf[(m - 1) * 32 + lane];
+            if (!(x > p.x + xtol(x))) {
+                // (near) zero-length piece: the previous vertex turns into slope s
+                // directly (reading A10, as pwl_device.cuh's Emit)
+                p.s = s;
+                if (m > 1 && buf[(m - 2) * 32 + lane].s == s) m--;  // no longer a kink
+                last_s = s;
+                return;
+            }
+        }
+        if (m >= STAGE) { err |= DEV_OVERFLOW; return; }
+        Vtx& o = buf[m * 32 + lane];
+        o.x = x; o.f = f; o.s = s;
+        m++;
+        last_s = s;
+    }
+};
+
+// Stage z's vertices strictly inside (a, b); a finite or -inf (then the state
+// at -inf is given: v = the M line, u = its lo line, zU0 = u wins there).
+// s_cur: z's slope just right of a.  Returns z's slope just left of b.
+template <class Out>
+__device__ __forceinline__ double emit_open(double a, double b, const Line& LW, const Line& LM, bool hasM,
+                                            const Line& LP, bool hasP, const PCtx& c, double s_cur, bool zU0,
+                                            Out& st) {
+    double pos = a;
+    int vi;
+    bool zU;
+    double zv;
+    if (isfinite(a)) z_side(LW, LM, hasM, LP, hasP, c, a, true, vi, zU, zv);
+    else { vi = hasM ? 1 : 0; zU = zU0; }
+    // events closer than xtol() to either end are rounding images of the end
+    // vertex itself (e.g. the M line passes through the vertex that defines it)
+    const double b_in = isfinite(b) ? b - xtol(b) : b;
+    for (int it = 0; it < 10; ++it) {
+        const Line V = vi == 0 ? LW : (vi == 1 ? LM : LP);
+        const double ref = isfinite(pos) ? pos : c.ux;
+        const double p_in = isfinite(pos) ? pos + xtol(pos) : pos;
+        const double us = (pos >= c.ux) ? c.hi : c.lo;
+        const Line Uq{c.ux, c.uf, us};
+        double nx = b_in;
+        // v switches to a line with a smaller slope that comes from above
+        if (vi != 1 && hasM && LM.s < V.s) { const double y = cross_at(LM, V, ref); if (y > p_in && y < nx) nx = y; }
+        if (vi != 2 && hasP && LP.s < V.s) { const double y = cross_at(LP, V, ref); if (y > p_in && y < nx) nx = y; }
+        if (vi != 0 && LW.s < V.s) { const double y = cross_at(LW, V, ref); if (y > p_in && y < nx) nx = y; }
+        // u's kink
+        if (pos < c.ux && c.ux < nx) nx = c.ux;
+        // z's loser overtakes the winner
+        {
+            const Line& Wn = zU ? Uq : V;
+            const Line& Ls = zU ? V : Uq;
+            if (c.seller ? (Ls.s > Wn.s) : (Ls.s < Wn.s)) {
+                const double y = cross_at(Ls, Wn, ref);
+                if (y > p_in && y < nx) nx = y;
+            }
+        }
+        if (!(nx < b_in)) break;
+        pos = nx;
+        const double s_new = z_side(LW, LM, hasM, LP, hasP, c, pos, true, vi, zU, zv);
+        if (s_new != s_cur) {
+            st.push(pos, zv, s_new);
+            s_cur = s_new;
+        }
+    }
+    return s_cur;
+}
+
+// warp-level scans
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(FULLM, v, o));
+    return v;
+}
+// exclusive suffix min over lanes > lane
+__device__ __forceinline__ double excl_suffix_min(double v, int lane) {
+    double x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_down_sync(FULLM, x, o);
+        if (lane + o < 32) x = fmin(x, y);
+    }
+    const double nx = __shfl_down_sync(FULLM, x, 1);
+    return lane < 31 ? nx : INFINITY;
+}
+// exclusive prefix min over lanes < lane
+__device__ __forceinline__ double excl_prefix_min(double v, int lane) {
+    double x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(FULLM, x, o);
+        if (lane >= o) x = fmin(x, y);
+    }
+    const double px = __shfl_up_sync(FULLM, x, 1);
+    return lane > 0 ? px : INFINITY;
+}
+__device__ __forceinline__ int excl_prefix_sum(int v, int lane, int& total) {
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULLM, x, o);
+        if (lane >= o) x += y;
+    }
+    total = __shfl_sync(FULLM, x, 31);
+    return x - v;
+}
+
+// ---------------------------------------------------------------------------
+// the heavy node update
+//   scratch: >= 2 * ceil(nE/32) doubles + STAGE * 32 vertices (global, per warp)
+//   output:  Z appended to arena at *counter (the caller's bump counter for this
+//            arena; only this warp allocates from it meanwhile)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ size_t scratch_vertices(int nE) {
+    const int nb = (nE + 31) / 32;
+    return (size_t)STAGE * 32 + (size_t)(2 * nb * sizeof(double) + sizeof(Vtx) - 1) / sizeof(Vtx) + 1;
+}
+
+__device__ __noinline__ int node_update_chunk(const Fn U, const Fn D, double lo, double hi, double ux, double uf,
+                                              bool seller, Vtx* scratch, int scap, Vtx* arena, int* counter,
+                                              int acap, int& zoff, int& nZ, int lane) {
+    const HCtx h = make_ctx(U, D);
+    const int nb = (h.nE + 31) / 32;
+    if ((size_t)scap < scratch_vertices(h.nE)) return DEV_OVERFLOW;
+    Vtx* stage_buf = scratch;
+    double* Mafter = reinterpret_cast<double*>(scratch + STAGE * 32);
+    double* Xafter = Mafter + nb;
+    // restriction is finite iff W's tails are steeper than the quotes (d < r < u)
+    {
+        const double sWr = h.wInf_U ? U.v(U.n - 1).s : D.v(D.n - 1).s;
+        const double sWl = h.tailL_U ? U.sl : D.sl;
+        if (sWr < lo || sWl > hi) return DEV_UNBOUNDED;
+    }
+    // ---- sweep 1: right to left, suffix minima of g at block boundaries ----
+    {
+        double Mc = INFINITY, Xc = INFINITY;
+        for (int blk = nb - 1; blk >= 0; --blk) {
+            const BlockW B = block_w(h, blk, lane);
+            double gm = INFINITY, fx = INFINITY;
+            for (int q = 0; q < B.w.n; ++q) {
+                const WV w = B.w.get(q);
+                gm = fmin(gm, fma(-lo, w.x, w.f));
+                fx = fmin(fx, w.x);
+            }
+            if (lane == 0) {
+                Mafter[blk] = Mc;
+                Xafter[blk] = Xc;
+            }
+            Mc = fmin(Mc, warp_min(gm));
+            Xc = fmin(Xc, warp_min(fx));
+        }
+    }
+    __syncwarp();
+    // ---- sweep 2: left to right, emit z ----
+    const PCtx c{lo, hi, ux, uf, seller};
+    const int base = *counter;  // this warp's allocation point in the arena
+    int total = 0;
+    int err = DEV_OK;
+    double Pc = INFINITY;       // prefix min of h over earlier blocks
+    double s_in = lo;           // z's slope arriving from the left (z's left tail is lo)
+    bool any_before = false;    // a W vertex in an earlier block
+    double last_x = -INFINITY;  // the last vertex written (earlier blocks)
+    for (int blk = 0; blk < nb; ++blk) {
+        const BlockW B = block_w(h, blk, lane);
+        const int nw = B.w.n;
+        // lane aggregates
+        double gl = INFINITY, hl = INFINITY, fx = INFINITY;
+        for (int q = 0; q < nw; ++q) {
+            const WV w = B.w.get(q);
+            gl = fmin(gl, fma(-lo, w.x, w.f));
+            hl = fmin(hl, fma(-hi, w.x, w.f));
+            fx = fmin(fx, w.x);
+        }
+        const double Mr = fmin(excl_suffix_min(gl, lane), Mafter[blk]);  // g over lanes > lane and later blocks
+        const double Pl = fmin(excl_prefix_min(hl, lane), Pc);           // h over lanes < lane and earlier blocks
+        const double Xr = fmin(excl_suffix_min(fx, lane), Xafter[blk]);  // next W vertex after this lane
+        int cntb;
+        const int before = excl_prefix_sum(nw > 0 ? 1 : 0, lane, cntb);
+        const bool first_overall = !any_before && before == 0 && nw > 0;
+        // suffix minima for own vertices: M after vertex q
+        double Mq2 = Mr, Mq1 = Mr, Mq0 = Mr;  // M_{j+1} for own vertices 2, 1, 0
+        {
+            if (nw >= 3) Mq1 = fmin(Mr, fma(-lo, B.w.v2.x, B.w.v2.f));
+            if (nw >= 2) Mq0 = fmin(nw >= 3 ? Mq1 : Mr, fma(-lo, B.w.v1.x, B.w.v1.f));
+            if (nw == 2) Mq1 = Mr;
+        }
+        Stage st;
+        st.buf = stage_buf;
+        st.lane = lane;
+        st.m = 0;
+        st.err = DEV_OK;
+        st.last_s = NAN;
+        double P = Pl;
+        double s_run = NAN;    // z's slope just left of the current position (NaN: from the left lane)
+        bool pending = false;  // stage slot 0 is a candidate to check against that slope
+        for (int q = 0; q < nw; ++q) {
+            const WV w = B.w.get(q);
+            const double Mnext = q == 0 ? Mq0 : (q == 1 ? Mq1 : Mq2);
+            const double Mj = fmin(fma(-lo, w.x, w.f), Mnext);
+            const double xn = (q + 1 < nw) ? B.w.get(q + 1).x : Xr;
+            if (q == 0 && first_overall) {
+                // left-tail piece (-inf, x_0): v = min(W tail, lo y + M_0); far left v is
+                // the M line and u its lo line (parallel): the winner is decided by value
+                const Line LW{w.x, w.f, w.sL}, LM{0.0, Mj, lo}, LP{0.0, INFINITY, hi};
+                const double mv = LM.at(ux);
+                const double tl = ftol(mv, uf);
+                const bool zU0 = fabs(uf - mv) > tl ? (seller ? uf > mv : uf < mv) : false;
+                s_run = emit_open(-INFINITY, w.x, LW, LM, true, LP, false, c, lo, zU0, st);
+            }
+            // the vertex at x_j: z's slope just right of it
+            int vi;
+            bool zU;
+            double zv;
+            const double Pj = fmin(P, fma(-hi, w.x, w.f));
+            const Line LWr{w.x, w.f, w.sR}, LMr{0.0, Mnext, lo}, LPr{0.0, Pj, hi};
+            const double sr_ = z_side(LWr, LMr, isfinite(Mnext), LPr, true, c, w.x, true, vi, zU, zv);
+            if (s_run != s_run) {  // unknown: decided once the left lane's slope is known
+                pending = st.m == 0;
+                st.push(w.x, zv, sr_);
+            } else if (sr_ != s_run) {
+                st.push(w.x, zv, sr_);
+            }
+            s_run = emit_open(w.x, xn, LWr, LMr, isfinite(Mnext), LPr, true, c, sr_, false, st);
+            P = Pj;
+        }
+        const double s_end = s_run;
+        // the slope arriving from the left: z's slope at the end of the nearest
+        // earlier lane with W vertices (or of the previous block)
+        double s_left = s_in;
+        {
+            int src = nw > 0 ? lane : -1;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(FULLM, src, o);
+                if (lane >= o) src = max(src, y);
+            }
+            int srcp = __shfl_up_sync(FULLM, src, 1);
+            if (lane == 0) srcp = -1;
+            const double se = __shfl_sync(FULLM, s_end, srcp < 0 ? 0 : srcp);
+            if (srcp >= 0) s_left = se;
+            const int lastsrc = __shfl_sync(FULLM, src, 31);
+            const double se_last = __shfl_sync(FULLM, s_end, lastsrc < 0 ? 0 : lastsrc);
+            if (lastsrc >= 0) s_in = se_last;
+        }
+        // drop the pending candidate when z has no kink there
+        const int skip0 = (pending && stage_buf[lane].s == s_left) ? 1 : 0;
+        err |= __reduce_or_sync(FULLM, st.err);
+        int cnt = st.m - skip0;
+        // fold across lanes (as Emit does within one): a first vertex closer than
+        // xtol() to the previous kept vertex is merged into it (that vertex takes
+        // its slope), so rounding-made micro-pieces never accumulate
+        double f0x = 0.0, fs = 0.0, lx = -INFINITY;
+        if (cnt > 0) {
+            f0x = stage_buf[skip0 * 32 + lane].x;
+            fs = stage_buf[skip0 * 32 + lane].s;
+            lx = stage_buf[(st.m - 1) * 32 + lane].x;
+        }
+        int prevl = cnt > 0 ? lane : -1;  // nearest lane <= this one with vertices
+        int nextl = cnt > 0 ? lane : 32;  // nearest lane >= this one with vertices
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULLM, prevl, o);
+            if (lane >= o) prevl = max(prevl, y);
+            const int z = __shfl_down_sync(FULLM, nextl, o);
+            if (lane + o < 32) nextl = min(nextl, z);
+        }
+        int pl = __shfl_up_sync(FULLM, prevl, 1);
+        if (lane == 0) pl = -1;
+        int nl = __shfl_down_sync(FULLM, nextl, 1);
+        if (lane == 31) nl = 32;
+        const double px = __shfl_sync(FULLM, lx, pl < 0 ? 0 : pl);
+        const double prev_x = pl < 0 ? last_x : px;
+        const bool fold = cnt > 0 && !(f0x > prev_x + xtol(f0x));
+        const int nfold = __shfl_sync(FULLM, (int)fold, nl > 31 ? 0 : nl);
+        const double nfs = __shfl_sync(FULLM, fs, nl > 31 ? 0 : nl);
+        if (cnt > 0 && nl <= 31 && nfold) stage_buf[(st.m - 1) * 32 + lane].s = nfs;  // absorb the next lane's first
+        if (fold && pl < 0 && total > 0) arena[base + total - 1].s = fs;               // into the previous block
+        const int drop_first = (fold && (pl >= 0 || total > 0)) ? 1 : 0;
+        cnt -= drop_first;
+        int tot;
+        const int off = excl_prefix_sum(cnt, lane, tot);
+        if (base + total + tot > acap) err |= DEV_OVERFLOW;
+        if (err) break;
+        for (int q = 0; q < cnt; ++q)
+            arena[base + total + off + q] = stage_buf[(q + skip0 + drop_first) * 32 + lane];
+        total += tot;
+        {
+            const int lastl = __shfl_sync(FULLM, prevl, 31);
+            const double lxl = __shfl_sync(FULLM, lx, lastl < 0 ? 0 : lastl);
+            if (lastl >= 0) last_x = lxl;
+        }
+        Pc = fmin(Pc, warp_min(hl));
+        any_before = any_before || (cntb > 0);
+        __syncwarp();
+    }
+    if (!err && total == 0) {
+        // z is a single line (cannot happen for a heavy node; kept for safety)
+        if (base + 1 > acap) err |= DEV_OVERFLOW;
+        else if (lane == 0) arena[base] = Vtx{0.0, fma(lo, -ux, uf), lo};
+        total = 1;
+    }
+    if (lane == 0 && !err) *counter = base + total;
+    __syncwarp();
+    zoff = base;
+    nZ = total;
+    return err;
+}
+
+
+// ===========================================================================
+// Lane-contiguous heavy update (the default): lane i runs a sequential,
+// forward W generator over its own segment of the merged event sequence
+// (carried merge state, as the per-lane node update does), so the per-event
+// cost is that of the sequential algorithm; the segments are joined by warp
+// scans (suffix minima of g, prefix minima of h, look-ahead to the next W
+// vertex, the slope arriving from the left) and a count-then-write pass.
+// M_{j+1} = min over later W vertices of g: inside a lane it is g_{j+1} or the
+// value at a later local minimum of g (recorded in pass 1; at most LMAX).
+// Anything unusual (too many local minima, a fold into a dropped vertex)
+// falls back to node_update_chunk.
+// ===========================================================================
+constexpr int LMAX = 6;
+
+// forward W generator over merged events [k, kend)
+struct WGen {
+    const Fn* U;
+    const Fn* D;
+    int k, kend, a;      // next event, end, U events before k
+    double x_prev;       // position of the previous event
+    bool wRp;            // winner (U?) just right of the previous event
+    int klast;
+    bool wInf;
+    // pending vertices of the current event (up to 3)
+    WV3 cur;
+    int q;
+
+    __device__ __forceinline__ void init(const HCtx& h, int k0, int k1, int lane_dummy) {
+        U = &h.U;
+        D = &h.D;
+        k = k0;
+        kend = k1;
+        klast = h.klast;
+        wInf = h.wInf_U;
+        a = split(h.U, h.D, k0, 0, h.U.n);
+        if (k0 == 0) {
+            x_prev = -INFINITY;
+            wRp = h.tailL_U;
+        } else {
+            const int ap = split(h.U, h.D, k0 - 1, max(a - 1, 0), a);
+            const Ev ep = event_at(h.U, h.D, k0 - 1, ap);
+            x_prev = ep.x;
+            wRp = winR(ep);
+        }
+        cur.n = 0;
+        q = 0;
+        (void)lane_dummy;
+    }
+    // next W vertex; false at the end of the segment
+    __device__ __forceinline__ bool next(WV& w) {
+        while (q >= cur.n) {
+            if (k >= kend) return false;
+            const Ev e = event_at(*U, *D, k, a);
+            cur = w_vertices(e, true, x_prev, wRp, k == klast, wInf);
+            q = 0;
+            // advance the merge position: event k consumed one vertex of U or D
+            const int b = k - a;
+            const bool isU = a < U->n && (b >= D->n || U->v(a).x <= D->v(b).x);
+            a += isU ? 1 : 0;
+            x_prev = e.x;
+            wRp = winR(e);
+            ++k;
+        }
+        w = cur.get(q++);
+        return true;
+    }
+};
+
+// register emitter: in-lane folding (as Emit) with the previous vertex kept
+// in registers; out == nullptr counts only
+struct LEmit {
+    Vtx* out;
+    int m;
+    bool have;
+    double lx, ls;   // last vertex written: x and slope
+    double ps;       // slope before the last vertex (NaN if unknown)
+    int err;
+    __device__ __forceinline__ void push(double x, double f, double s) {
+        if (have && !(x > lx + xtol(x))) {  // (near) zero-length piece
+            if (m == 1) err |= 8;  // folded into the first vertex (may be dropped): bail out
+            if (out) out[m - 1].s = s;
+            ls = s;
+            if (ps == s) err |= 4;  // the fold made the last vertex a non-kink: rare, bail out
+            return;
+        }
+        if (out) out[m] = Vtx{x, f, s};
+        m++;
+        ps = have ? ls : NAN;
+        have = true;
+        lx = x;
+        ls = s;
+    }
+};
+
+// emission of z for the W vertex w and its right piece, shared by the count and
+// write passes.  Returns z's slope at the end of the piece.
+struct EmitAdapter {
+    LEmit* e;
+    __device__ __forceinline__ void push(double x, double f, double s) { e->push(x, f, s); }
+};
+
+__device__ __noinline__ int node_update(const Fn U, const Fn D, double lo, double hi, double ux, double uf,
+                                        bool seller, Vtx* scratch, int scap, Vtx* arena, int* counter, int acap,
+                                        int& zoff, int& nZ, int lane) {
+    const HCtx h = make_ctx(U, D);
+    {
+        const double sWr = h.wInf_U ? U.v(U.n - 1).s : D.v(D.n - 1).s;
+        const double sWl = h.tailL_U ? U.sl : D.sl;
+        if (sWr < lo || sWl > hi) return DEV_UNBOUNDED;
+    }
+    // segments: lane i owns events [k0, k1)
+    const int nE = h.nE;
+    const int k0 = (int)(((long long)nE * lane) / 32), k1 = (int)(((long long)nE * (lane + 1)) / 32);
+    // ---- pass 1: W vertices of the segment: g / h minima, first vertex, local minima of g ----
+    double gmin = INFINITY, hmin = INFINITY, fx = INFINITY, fg = INFINITY;
+    int nw = 0;
+    double lmx[LMAX], lmg[LMAX];  // local minima of g (x, g), in order
+    int nlm = 0;
+    int fail = 0;
+    {
+        WGen G;
+        G.init(h, k0, k1, lane);
+        WV w;
+        double gprev = INFINITY, xprev = 0.0;
+        bool desc = false;  // g was decreasing into the previous vertex
+        while (G.next(w)) {
+            const double g = fma(-lo, w.x, w.f), hh = fma(-hi, w.x, w.f);
+            if (nw == 0) { fx = w.x; fg = g; }
+            gmin = fmin(gmin, g);
+            hmin = fmin(hmin, hh);
+            // the previous vertex is a local minimum of g when g stops decreasing there
+            if (nw > 0 && desc && !(g < gprev)) {
+                if (nlm < LMAX) {
+#pragma unroll
+                    for (int i = 0; i < LMAX; ++i)
+                        if (i == nlm) { lmx[i] = xprev; lmg[i] = gprev; }
+                    nlm++;
+                } else {
+                    fail = 1;
+                }
+            }
+            desc = nw > 0 ? (g < gprev) : true;
+            gprev = g;
+            xprev = w.x;
+            nw++;
+        }
+        // the last vertex ends a descent: a local minimum within the lane
+        if (nw > 0 && desc) {
+            if (nlm < LMAX) {
+#pragma unroll
+                for (int i = 0; i < LMAX; ++i)
+                    if (i == nlm) { lmx[i] = xprev; lmg[i] = gprev; }
+                nlm++;
+            } else {
+                fail = 1;
+            }
+        }
+    }
+    // suffix minima over the recorded local minima (lmg[i] = min over i..nlm-1)
+#pragma unroll
+    for (int i = LMAX - 2; i >= 0; --i)
+        if (i + 1 < nlm) lmg[i] = fmin(lmg[i], lmg[i + 1]);
+    if (__any_sync(FULLM, fail))
+        return node_update_chunk(U, D, lo, hi, ux, uf, seller, scratch, scap, arena, counter, acap, zoff, nZ, lane);
+    // ---- scans ----
+    const double Mr = excl_suffix_min(gmin, lane);   // g over later lanes
+    const double Pl = excl_prefix_min(hmin, lane);   // h over earlier lanes
+    // next W vertex after this lane: first vertex of the nearest later non-empty lane
+    int nxt = nw > 0 ? lane : 32;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_down_sync(FULLM, nxt, o);
+        if (lane + o < 32) nxt = min(nxt, y);
+    }
+    int nl = __shfl_down_sync(FULLM, nxt, 1);
+    if (lane == 31) nl = 32;
+    const double Xs = __shfl_sync(FULLM, fx, nl < 32 ? nl : 0);  // (every lane shuffles)
+    const double Xr = nl < 32 ? Xs : INFINITY;
+    int before;
+    {
+        int tot;
+        before = excl_prefix_sum(nw > 0 ? 1 : 0, lane, tot);
+    }
+    const bool first_overall = before == 0 && nw > 0;
+    const PCtx c{lo, hi, ux, uf, seller};
+
+    // ---- pass 2 (twice: count, then write) ----
+    int cnt = 0, drop = 0, off = 0, total = 0;
+    double s_end = NAN, first_s = NAN;
+    bool pend_first = false;
+    bool folded_first = false;
+    const int base = *counter;
+    for (int pass = 0; pass < 2; ++pass) {
+        LEmit E;
+        // this lane's region starts at arena[base + off]; a dropped first candidate
+        // would sit just before it and is never written
+        E.out = pass ? arena + base + off - drop : nullptr;
+        E.m = 0;
+        E.have = false;
+        E.ps = NAN;
+        E.err = DEV_OK;
+        WGen G;
+        G.init(h, k0, k1, lane);
+        WV w, wn;
+        bool has = G.next(w);
+        double P = Pl;
+        double s_run = NAN;
+        int li = 0;  // next local minimum index (by position)
+        bool first = true;
+        while (has) {
+            const bool hasn = G.next(wn);
+            const double xn = hasn ? wn.x : Xr;
+            // M after w: g at the next W vertex, later local minima, later lanes
+            while (li < nlm && !(lmx[li > LMAX - 1 ? LMAX - 1 : li] > w.x)) ++li;
+            double Mnext = Mr;
+            if (hasn) Mnext = fmin(Mnext, fma(-lo, wn.x, wn.f));
+            if (li < nlm) {
+                double lv = INFINITY;
+#pragma unroll
+                for (int i = 0; i < LMAX; ++i)
+                    if (i == li) lv = lmg[i];
+                Mnext = fmin(Mnext, lv);
+            }
+            const double Mj = fmin(fma(-lo, w.x, w.f), Mnext);
+            LEmit* Ep = &E;
+            EmitAdapter ad{Ep};
+            if (first && first_overall) {
+                const Line LW{w.x, w.f, w.sL}, LM{0.0, Mj, lo}, LP{0.0, INFINITY, hi};
+                const double mv = LM.at(ux);
+                const double tl = ftol(mv, uf);
+                const bool zU0 = fabs(uf - mv) > tl ? (seller ? uf > mv : uf < mv) : false;
+                s_run = emit_open(-INFINITY, w.x, LW, LM, true, LP, false, c, lo, zU0, ad);
+            }
+            int vi;
+            bool zU;
+            double zv;
+            const double Pj = fmin(P, fma(-hi, w.x, w.f));
+            const Line LWr{w.x, w.f, w.sR}, LMr{0.0, Mnext, lo}, LPr{0.0, Pj, hi};
+            const double sr_ = z_side(LWr, LMr, isfinite(Mnext), LPr, true, c, w.x, true, vi, zU, zv);
+            if (s_run != s_run) {  // unknown: checked against the left lane's slope
+                if (pass == 0) { pend_first = E.m == 0; first_s = sr_; }
+                if (!(pass == 1 && drop && E.m == 0 && !E.have)) E.push(w.x, zv, sr_);
+                else { E.have = true; E.lx = w.x; E.ls = sr_; E.ps = NAN; E.m = 1; }
+            } else if (sr_ != s_run) {
+                E.push(w.x, zv, sr_);
+            }
+            s_run = emit_open(w.x, xn, LWr, LMr, isfinite(Mnext), LPr, true, c, sr_, false, ad);
+            P = Pj;
+            w = wn;
+            has = hasn;
+            first = false;
+        }
+        // a fold into a first vertex matters only when that vertex is dropped
+        // (checked below, once drop is known)
+        const bool fold8 = (E.err & 8) != 0;
+        E.err &= ~8;
+        if (__any_sync(FULLM, E.err))
+            return node_update_chunk(U, D, lo, hi, ux, uf, seller, scratch, scap, arena, counter, acap, zoff, nZ,
+                                     lane);
+        if (pass == 0) {
+            folded_first = fold8;
+            cnt = E.m;
+            s_end = s_run;
+            // the slope arriving from the left: s_end of the nearest earlier non-empty lane
+            int src = nw > 0 ? lane : -1;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(FULLM, src, o);
+                if (lane >= o) src = max(src, y);
+            }
+            int srcp = __shfl_up_sync(FULLM, src, 1);
+            if (lane == 0) srcp = -1;
+            const double se = __shfl_sync(FULLM, s_end, srcp < 0 ? 0 : srcp);
+            const double s_left = srcp >= 0 ? se : lo;  // z's left tail slope is lo
+            drop = (pend_first && !first_overall && first_s == s_left) ? 1 : 0;
+            if (__any_sync(FULLM, drop && folded_first))
+                return node_update_chunk(U, D, lo, hi, ux, uf, seller, scratch, scap, arena, counter, acap, zoff,
+                                         nZ, lane);
+            cnt -= drop;
+            off = excl_prefix_sum(cnt, lane, total);
+            if (base + total > acap) return DEV_OVERFLOW;
+        }
+    }
+    __syncwarp();
+    if (total == 0) {
+        if (base + 1 > acap) return DEV_OVERFLOW;
+        if (lane == 0) arena[base] = Vtx{0.0, fma(lo, -ux, uf), lo};
+        total = 1;
+    }
+    if (lane == 0) *counter = base + total;
+    __syncwarp();
+    zoff = base;
+    nZ = total;
+    return DEV_OK;
+}
+
+// a6 helper: min over the vertices b of W = max(U, D) of W(b) + S0 b, and W's
+// tail slopes (for the boundedness check)
+__device__ __noinline__ double root_min(const Fn U, const Fn D, double S0, double& slW, double& srW, int lane) {
+    const HCtx h = make_ctx(U, D);
+    const int nb = (h.nE + 31) / 32;
+    double mv = INFINITY;
+    for (int blk = 0; blk < nb; ++blk) {
+        const BlockW B = block_w(h, blk, lane);
+        for (int q = 0; q < B.w.n; ++q) {
+            const WV w = B.w.get(q);
+            mv = fmin(mv, fma(S0, w.x, w.f));
+        }
+    }
+    slW = h.tailL_U ? U.sl : D.sl;
+    srW = h.wInf_U ? U.v(U.n - 1).s : D.v(D.n - 1).s;
+    return warp_min(mv);
+}
+
+}  // namespace heavy
+}  // namespace amtc

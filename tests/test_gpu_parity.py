@@ -175,3 +175,40 @@ def test_crr_equals_tc_at_k0(api):
     assert rc == 0
     np.testing.assert_allclose(tc["ask"], crr, rtol=RTOL, atol=ATOL)
     np.testing.assert_allclose(tc["bid"], crr, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("tl", [2, 5, 12])
+def test_warp_path_forced(api, tl):
+    """Force the warp-cooperative (heavy) node update onto ordinary nodes and
+    check it against the oracle (the testing hook of include/amtc.h)."""
+    b = W.random_small(40, seed=4000 + tl, k_max=0.08)
+    ref, rc0 = api.price_american_tc_batch_host(b, 45)
+    try:
+        api.debug_set_heavy_threshold(tl)
+        got, rc = api.price_american_tc_batch_host(b, 45)
+    finally:
+        api.debug_set_heavy_threshold(0)
+    assert rc == 0 and rc0 == 0
+    assert_quotes(got, b, 45)
+    # the warp path keeps representations as lean as the lane path
+    assert np.all(got["max_bp"] <= ref["max_bp"] + 4), (got["max_bp"], ref["max_bp"])
+
+
+def test_heavy_sawtooth_calls(api):
+    """Calls at large k/h: the buyer's node functions grow to hundreds of
+    vertices (the warp path without forcing)."""
+    b = W.random_small(12, seed=99, k_max=0.0)
+    b.kind[:] = 1
+    b.K[:] = np.linspace(90.0, 115.0, 12)
+    b.k[:] = np.linspace(0.006, 0.02, 12)
+    b.T[:] = 0.6
+    b.sigma[:] = 0.3
+    N = 400
+    got, rc = api.price_american_tc_batch_host(b, N)
+    assert rc == 0
+    assert got["max_bp"].max() > 64  # the warp path ran
+    want = [O.price_tc(_opt(b.row(i)), N) for i in range(len(b))]
+    assert_quotes(got, b, N, want)
+    # no representation bloat: vertex counts as in the oracle (kinks + 1), small slack
+    for i, q in enumerate(want):
+        assert got["max_bp"][i] <= 1.1 * (max(q.max_kinks_ask, q.max_kinks_bid) + 1) + 4, (i, got["max_bp"][i], q)
