@@ -52,14 +52,14 @@ struct StripLayout {
     size_t epow, dpow;          // 2N+3 / N+2 doubles: e^{h (i-(N+1))}, e^{-rho t}
     size_t chdr, csl, cv;       // carry column: header (n, arena offset | -1), left slope, C inline vertices
     size_t carena, rarena;      // carry arena (per strip parity), row arena (per level parity)
-    size_t lscr, hscr;          // tier-2 lane scratch (32 x 2 x BG), tier-3 warp scratch
+    size_t lscr, hscr, zbuf;    // tier-2 lane scratch (32 x 2 x BG), tier-3 warp scratch, tier-3 output
     size_t chdr_ps, csl_ps, cv_ps, carena_ps, rarena_ps;
     size_t total;
 };
 
 struct StripCaps {
     int C, B, BG, TL;
-    int carena_cap, rarena_cap, hscr_cap;
+    int carena_cap, rarena_cap, hscr_cap, zbuf_cap;
 };
 
 __host__ __device__ inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
@@ -83,9 +83,20 @@ static StripLayout strip_layout(int N, const StripCaps& c) {
     L.rarena = take(2 * L.rarena_ps);
     L.lscr = take(sizeof(Vtx) * (size_t)SW * 2 * c.BG);
     L.hscr = take(sizeof(Vtx) * (size_t)c.hscr_cap);
+    L.zbuf = take(sizeof(Vtx) * (size_t)c.zbuf_cap);
     L.total = p;
     return L;
 }
+
+// a heavy node posted by one lane for the CTA's warps (tier 3 work sharing)
+struct HMail {
+    const Vtx* up;
+    const Vtx* dp;
+    double usl, dsl, lo, hi, ux, uf;
+    int un, dn;
+    short ustr, dstr;
+    int res_err, res_n, res_off;
+};
 
 // per-warp shared memory
 template <int C, int B>
@@ -93,9 +104,21 @@ struct StripSmem {
     Vtx row[C * SW];  // lane-interleaved slots: vertex i of lane l at row[i * 32 + l]
     Vtx s0[B * SW];   // lane-interleaved scratch of the node update (A of pass 1)
     Vtx leaf31;       // lane 31's down child at t = N (an analytic leaf)
+    heavy::HWin hw;   // merge windows of the tier-3 (heavy) node update
+    HMail mail[SW];   // this warp's posted heavy nodes (one per lane)
+    Vtx* h_arena;     // where their results go (this warp's next row arena) ...
+    int* h_counter;   // ... and its bump counter
+    int h_acap, h_seller;
+    unsigned post;    // posted, not yet claimed heavy lanes
+    int done;         // posted, not yet completed
     int rcnt[2];      // row arena bump counters
     int ccnt;         // carry arena bump counter (current strip)
-    int pad;
+    int zcnt;         // scratch counter of the fallback heavy update
+};
+
+struct CtaHdr {
+    int active;  // warps of this CTA still working on items
+    int pad[3];
 };
 
 struct StripLaunch {
@@ -133,25 +156,71 @@ __device__ __forceinline__ Fn shfl_fn(const Fn& F, int src) {
     return G;
 }
 
-// tier 3: the warp updates every heavy node of this level, one after another
-// (pwl_heavy.cuh); results go to the row arena.  Out of line: rare.
-// Returns (status bits, this lane's result count, its arena offset).
-__device__ __noinline__ int3 heavy_phase(unsigned hmask, Fn U, Fn D, double lo, double hi, double ux, double uf,
-                                         bool seller, Vtx* hscr, int hcap, Vtx* arena, int* counter, int acap,
-                                         int lane) {
-    int3 res = make_int3(DEV_OK, 0, 0);
-    while (hmask) {
-        const int hl = __ffs(hmask) - 1;
-        hmask &= hmask - 1;
-        const Fn Uh = shfl_fn(U, hl), Dh = shfl_fn(D, hl);
-        const double hlo = __shfl_sync(FULL, lo, hl), hhi = __shfl_sync(FULL, hi, hl);
-        const double hux = __shfl_sync(FULL, ux, hl), huf = __shfl_sync(FULL, uf, hl);
-        int zoff = 0, zn = 0;
-        const int e = heavy::node_update(Uh, Dh, hlo, hhi, hux, huf, seller, hscr, hcap, arena, counter, acap, zoff,
-                                         zn, lane);
-        if (lane == hl) res = make_int3(e, zn, zoff);
+// tier 3 (work sharing inside the CTA): a warp whose level has heavy nodes
+// posts them (HMail per lane, bit mask `post`) and then serves posted nodes --
+// its own or any other warp's -- until its own are done; every warp also
+// serves one posted node per level of its own sweep, and warps without items
+// serve until the CTA is idle.  A claimed node is updated by the whole warp
+// (pwl_heavy.cuh) into the claimer's scratch and copied into the owner's row
+// arena.  Returns true if a node was served.
+template <int C, int B, int WARPS>
+__device__ __noinline__ bool serve_one(StripSmem<C, B>* all, int me, Vtx* hscr, int hcap, Vtx* zbuf, int zcap,
+                                       int lane) {
+    // candidate owner: the first warp (starting with this one) with posted nodes
+    unsigned pw = 0;
+    if (lane < WARPS) pw = *(volatile unsigned*)&all[(me + lane) % WARPS].post;
+    unsigned cand = __ballot_sync(FULL, pw != 0);
+    int owner = -1, ol = -1;
+    while (cand && owner < 0) {
+        const int c = __ffs(cand) - 1;
+        cand &= cand - 1;
+        const int w = (me + c) % WARPS;
+        int got = -1;
+        if (lane == 0) {
+            unsigned cur = *(volatile unsigned*)&all[w].post;
+            while (cur) {
+                const unsigned bit = cur & (0u - cur);
+                const unsigned old = atomicAnd(&all[w].post, ~bit);
+                if (old & bit) { got = __ffs(bit) - 1; break; }
+                cur = old & ~bit;
+            }
+        }
+        got = __shfl_sync(FULL, got, 0);
+        if (got >= 0) { owner = w; ol = got; }
     }
-    return res;
+    if (owner < 0) return false;
+    StripSmem<C, B>& O = all[owner];
+    const HMail& M = O.mail[ol];
+    const Fn U = make_fn(M.up, M.un, M.usl, M.ustr), D = make_fn(M.dp, M.dn, M.dsl, M.dstr);
+    const bool seller = O.h_seller != 0;
+    int nZ = 0;
+    int e = heavy::node_update_block(U, D, M.lo, M.hi, M.ux, M.uf, seller, &all[me].hw, hscr, hcap, zbuf, zcap, nZ,
+                                     lane);
+    if (e == heavy::DEV_FALLBACK) {  // rare shapes: the lane-contiguous update
+        if (lane == 0) all[me].zcnt = 0;
+        __syncwarp();
+        int zoff = 0;
+        e = heavy::node_update(U, D, M.lo, M.hi, M.ux, M.uf, seller, hscr, hcap, zbuf, &all[me].zcnt, zcap, zoff, nZ,
+                               lane);
+    }
+    int off = 0;
+    if (!e) {
+        if (lane == 0) off = atomicAdd(O.h_counter, nZ);
+        off = __shfl_sync(FULL, off, 0);
+        if (off + nZ > O.h_acap) e = DEV_OVERFLOW;
+        else
+            for (int i = lane; i < nZ; i += 32) O.h_arena[off + i] = zbuf[i];
+    }
+    __syncwarp();
+    if (lane == 0) {
+        O.mail[ol].res_err = e;
+        O.mail[ol].res_n = nZ;
+        O.mail[ol].res_off = off;
+        __threadfence_block();
+        atomicSub(&O.done, 1);
+    }
+    __syncwarp();
+    return true;
 }
 
 // a6: root, t = 0, no costs (derived A.4): v_0(y) = min_b [w_0(b) + S0 b] - S0 y
@@ -176,11 +245,21 @@ template <int C, int B, int WARPS, int MINB>
 __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_constant__ StripLaunch L) {
     extern __shared__ __align__(16) char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    StripSmem<C, B>& S = reinterpret_cast<StripSmem<C, B>*>(smem_raw)[wib];
+    CtaHdr& H = *reinterpret_cast<CtaHdr*>(smem_raw);
+    StripSmem<C, B>* const all = reinterpret_cast<StripSmem<C, B>*>(smem_raw + sizeof(CtaHdr));
+    StripSmem<C, B>& S = all[wib];
     const int N = L.N;
     char* const wb = L.ws + (size_t)(blockIdx.x * WARPS + wib) * L.lay.total;
     double* const Epow = WS1(double, epow);
     double* const Dpow = WS1(double, dpow);
+    Vtx* const hscr = WS1(Vtx, hscr);
+    Vtx* const zbuf = WS1(Vtx, zbuf);
+    if (threadIdx.x == 0) H.active = WARPS;
+    if (lane == 0) {
+        S.post = 0u;
+        S.done = 0;
+    }
+    __syncthreads();
 
     for (;;) {
         int it = 0;
@@ -234,6 +313,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
             for (int t = N; t >= max(j0, 1); --t) {
                 const int nxt = cur ^ 1;
                 const bool active = j <= t;
+                // help: serve one heavy node posted by another warp of the CTA
+                {
+                    unsigned pw = 0;
+                    if (lane < WARPS) pw = *(volatile unsigned*)&all[lane].post;
+                    if (__any_sync(FULL, pw != 0))
+                        serve_one<C, B, WARPS>(all, wib, hscr, L.caps.hscr_cap, zbuf, L.caps.zbuf_cap, lane);
+                }
                 // children: up = own previous; down = lane+1's previous / carry / leaf
                 const int dn = __shfl_down_sync(FULL, my_n, 1);
                 const int doff = __shfl_down_sync(FULL, my_off, 1);
@@ -286,15 +372,38 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
                     }
                     if (heavy) where = 0;
                 }
-                // tier 3: warp-cooperative updates of this level's heavy nodes
+                // tier 3: post this level's heavy nodes to the CTA and serve until they are done
                 const unsigned hmask = __ballot_sync(FULL, heavy);
                 int h_n = 0, h_off = 0;
                 if (hmask) {
-                    const int3 hr = heavy_phase(hmask, U, D, lo, hi, ux, uf, seller, WS1(Vtx, hscr), L.caps.hscr_cap,
-                                                WS(Vtx, rarena, nxt), &S.rcnt[nxt], L.caps.rarena_cap, lane);
-                    err |= hr.x;
-                    h_n = hr.y;
-                    h_off = hr.z;
+                    if (heavy) {
+                        HMail& m = S.mail[lane];
+                        m.up = U.p; m.un = U.n; m.usl = U.sl; m.ustr = (short)U.stride;
+                        m.dp = D.p; m.dn = D.n; m.dsl = D.sl; m.dstr = (short)D.stride;
+                        m.lo = lo; m.hi = hi; m.ux = ux; m.uf = uf;
+                    }
+                    if (lane == 0) {
+                        S.h_arena = WS(Vtx, rarena, nxt);
+                        S.h_counter = &S.rcnt[nxt];
+                        S.h_acap = L.caps.rarena_cap;
+                        S.h_seller = seller ? 1 : 0;
+                        S.done = __popc(hmask);
+                    }
+                    __syncwarp();
+                    __threadfence_block();
+                    if (lane == 0) atomicOr(&S.post, hmask);
+                    __syncwarp();
+                    while (*(volatile int*)&S.done > 0) {
+                        if (!serve_one<C, B, WARPS>(all, wib, hscr, L.caps.hscr_cap, zbuf, L.caps.zbuf_cap, lane))
+                            __nanosleep(64);
+                    }
+                    __threadfence_block();
+                    if (heavy) {
+                        const volatile HMail& m = S.mail[lane];
+                        err |= m.res_err;
+                        h_n = m.res_n;
+                        h_off = m.res_off;
+                    }
                 }
                 __syncwarp();
                 // pass 2 writes Z over the previous row, which is dead now (every
@@ -389,14 +498,21 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
         }
         __syncwarp();
     }
+    // no items left: serve the CTA's remaining heavy nodes until every warp is done
+    if (lane == 0) atomicSub(&H.active, 1);
+    __syncwarp();
+    while (*(volatile int*)&H.active > 0) {
+        if (!serve_one<C, B, WARPS>(all, wib, hscr, L.caps.hscr_cap, zbuf, L.caps.zbuf_cap, lane)) __nanosleep(256);
+    }
 }
 
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-constexpr int STRIP_C = 6, STRIP_B = 8, STRIP_WARPS = 4, STRIP_MINB = 4;
+// one CTA of 16 warps per SM: the CTA is the work-sharing domain of tier 3
+constexpr int STRIP_C = 6, STRIP_B = 6, STRIP_WARPS = 16, STRIP_MINB = 1;
 #define STRIP_KERNEL strip_kernel<STRIP_C, STRIP_B, STRIP_WARPS, STRIP_MINB>
-constexpr size_t STRIP_SMEM = sizeof(StripSmem<STRIP_C, STRIP_B>) * STRIP_WARPS;
+constexpr size_t STRIP_SMEM = sizeof(CtaHdr) + sizeof(StripSmem<STRIP_C, STRIP_B>) * STRIP_WARPS;
 
 static int strip_set_smem() {
     static int done = 0;
@@ -421,9 +537,16 @@ StripCaps strip_caps(int N, int level) {
     c.TL = g_tl_override ? g_tl_override : 64;
     const int64_t mul = (int64_t)1 << (2 * level);
     auto clampi = [](int64_t v) { return (int)(v > ((int64_t)1 << 28) ? ((int64_t)1 << 28) : v); };
-    c.rarena_cap = clampi(mul * (32 * (int64_t)(N + 2) + 4096));
-    c.carena_cap = clampi(mul * (32 * (int64_t)(N + 2) + 4096));
-    c.hscr_cap = clampi(heavy::STAGE * 32 + mul * (2 * (int64_t)(N + 2) + 4096));
+    // arenas sized so that the heaviest config-4 items (call buyers at k/h ~ 15:
+    // ~16 heavy columns of up to ~3N vertices) never need a retry pass: the
+    // row arena holds one level of a strip, the carry arena every carried
+    // function of a strip (the band crosses a carry column for ~32 levels)
+    c.rarena_cap = clampi(mul * (64 * (int64_t)(N + 2) + 8192));
+    c.carena_cap = clampi(mul * (100 * (int64_t)(N + 2) + 8192));
+    // tier 3 scratch: stage + W (<= 2 (nU + nD) + 8 vertices; the sawtooth grows by
+    // two vertices per level, so nU, nD <= ~2N) + block minima
+    c.hscr_cap = clampi(heavy::STAGE * 32 + mul * (14 * (int64_t)(N + 2) + 4096));
+    c.zbuf_cap = clampi(mul * (6 * (int64_t)(N + 2) + 4096));
     return c;
 }
 

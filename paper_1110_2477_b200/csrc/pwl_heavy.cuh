@@ -26,6 +26,7 @@ namespace heavy {
 
 constexpr unsigned FULLM = 0xffffffffu;
 constexpr int STAGE = 40;  // staged output vertices per lane per block
+constexpr int DEV_FALLBACK = 8;  // node_update_block: use node_update for this node
 
 // merged event k: the k-th vertex of U and D by x (U first on ties)
 struct Ev {
@@ -862,6 +863,289 @@ __device__ __noinline__ int node_update(const Fn U, const Fn D, double lo, doubl
     if (lane == 0) *counter = base + total;
     __syncwarp();
     zoff = base;
+    nZ = total;
+    return DEV_OK;
+}
+
+// ===========================================================================
+// Block-synchronous heavy update (the default tier 3).  No binary search and
+// no dependent load chain touches global memory: every global access is a
+// coalesced 32-wide load or store.
+//   sweep A (left to right): the merged events of U and D in blocks of 32.
+//     Lane i loads U[a+i] and D[b+i] into a per-warp shared window (cursors a,
+//     b carried across blocks); each window element's merged position is its
+//     index plus its rank in the other window (a 5-step binary search in
+//     shared memory); lane k takes merged event k.  The vertices of W =
+//     max(U, D) are compacted into the scratch buffer Wb.
+//   sweep B (right to left over W in blocks of 32): Mafter[b] = min of
+//     g = W - lo x over the blocks after b.
+//   sweep C (left to right): lane i owns W vertex 32 b + i and emits z on its
+//     right piece: v = min(W, lo y + M_{j+1}, hi y + P_j) (header identity),
+//     z = OP(u, v); staging, de-duplication, folding and compaction as in
+//     node_update_chunk.
+// ===========================================================================
+struct HWin {
+    Vtx u[33], d[33];  // [0]: the vertex before the window (or the left-tail anchor); [1..32]: window
+    int ev[32];        // merged event k of the block: isU | idx << 1 | rank << 7
+};
+
+__device__ __forceinline__ int rank_lt(const Vtx* w, double x) {  // #{m < 32 : w[1+m].x < x}
+    int p = 0;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1)
+        if (w[p + s].x < x) p += s;  // w[p+s] = window element p+s-1
+    return p + (w[p + 1].x < x ? 1 : 0);
+}
+__device__ __forceinline__ int rank_le(const Vtx* w, double x) {  // #{m < 32 : w[1+m].x <= x}
+    int p = 0;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1)
+        if (w[p + s].x <= x) p += s;
+    return p + (w[p + 1].x <= x ? 1 : 0);
+}
+
+// event k of the current block (window state in Wn); a, b: cursors (global
+// indices of window element 0), for the left-slope of the first vertices
+__device__ __forceinline__ Ev block_event(const HWin& Wn, int code) {
+    Ev e;
+    e.skip = false;
+    const bool isU = code & 1;
+    const int idx = (code >> 1) & 63, r = code >> 7;
+    if (isU) {
+        const Vtx V = Wn.u[1 + idx];
+        e.x = V.x; e.eU = V.f; e.sUR = V.s; e.sUL = Wn.u[idx].s;
+        const Vtx P = Wn.d[r];
+        if (r < 32 && Wn.d[1 + r].x == e.x) {  // coincident vertices: one event
+            const Vtx Q = Wn.d[1 + r];
+            e.eD = Q.f; e.sDL = P.s; e.sDR = Q.s;
+        } else {
+            e.eD = fma(P.s, e.x - P.x, P.f); e.sDL = P.s; e.sDR = P.s;
+        }
+    } else {
+        const Vtx V = Wn.d[1 + idx];
+        e.x = V.x; e.eD = V.f; e.sDR = V.s; e.sDL = Wn.d[idx].s;
+        const Vtx P = Wn.u[r];
+        e.eU = fma(P.s, e.x - P.x, P.f); e.sUL = P.s; e.sUR = P.s;
+        if (P.x == e.x) {  // the U vertex at the same x handled both (r = 0: the previous block's)
+            e.skip = true;
+            e.eU = P.f; e.sUR = P.s; e.sUL = P.s;  // sUL unused for a skip
+        }
+    }
+    return e;
+}
+
+// z is written to zout[0 .. nZ) (contiguous, capacity zcap)
+template <class WinPtr>
+__device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo, double hi, double ux, double uf,
+                                              bool seller, WinPtr win, Vtx* scratch, int scap, Vtx* zout, int zcap,
+                                              int& nZ, int lane) {
+    Vtx* const arena = zout;
+    const int acap = zcap;
+    HWin& Wn = *win;
+    const HCtx h = make_ctx(U, D);
+    {
+        const double sWr = h.wInf_U ? U.v(U.n - 1).s : D.v(D.n - 1).s;
+        const double sWl = h.tailL_U ? U.sl : D.sl;
+        if (sWr < lo || sWl > hi) return DEV_UNBOUNDED;
+    }
+    const int nE = h.nE;
+    const int wcap = 2 * nE + 8;  // W: at most a crossing and a vertex per event, plus the right tail
+    const int nbmax = (wcap + 31) / 32;
+    if ((size_t)scap < (size_t)STAGE * 32 + (size_t)wcap + (size_t)nbmax + 2) return DEV_OVERFLOW;
+    (void)nbmax;
+    Vtx* const stage_buf = scratch;
+    Vtx* const Wb = scratch + STAGE * 32;
+    double* const Mafter = reinterpret_cast<double*>(Wb + wcap);
+
+    // ---- sweep A: W = max(U, D) into Wb ----
+    int a = 0, b = 0, nW = 0;
+    double cx = -INFINITY;   // x of the last event of the previous block
+    bool cwr = h.tailL_U;    // winner just right of it (first block: the left-tail winner)
+    if (lane == 0) {
+        Wn.u[0] = Vtx{U.v(0).x, U.v(0).f, U.sl};
+        Wn.d[0] = Vtx{D.v(0).x, D.v(0).f, D.sl};
+    }
+    for (int k0 = 0; k0 < nE; k0 += 32) {
+        Wn.u[1 + lane] = (a + lane < U.n) ? U.v(a + lane) : Vtx{INFINITY, 0.0, 0.0};
+        Wn.d[1 + lane] = (b + lane < D.n) ? D.v(b + lane) : Vtx{INFINITY, 0.0, 0.0};
+        __syncwarp();
+        const int nrem = min(32, nE - k0);
+        {
+            const Vtx uu = Wn.u[1 + lane], dd = Wn.d[1 + lane];
+            if (a + lane < U.n) {
+                const int r = rank_lt(Wn.d, uu.x);
+                const int pos = lane + r;
+                if (pos < nrem) Wn.ev[pos] = 1 | (lane << 1) | (r << 7);
+            }
+            if (b + lane < D.n) {
+                const int r = rank_le(Wn.u, dd.x);
+                const int pos = lane + r;
+                if (pos < nrem) Wn.ev[pos] = (lane << 1) | (r << 7);
+            }
+        }
+        __syncwarp();
+        const bool valid = lane < nrem;
+        const int code = valid ? Wn.ev[lane] : 0;
+        Ev e;
+        if (valid) e = block_event(Wn, code);
+        else { e.x = INFINITY; e.eU = e.eD = 0.0; e.sUL = e.sUR = e.sDL = e.sDR = 0.0; e.skip = true; }
+        const bool wr = valid ? winR(e) : false;
+        double x_prev = __shfl_up_sync(FULLM, e.x, 1);
+        bool wRp = __shfl_up_sync(FULLM, (int)wr, 1) != 0;
+        if (lane == 0) { x_prev = cx; wRp = cwr; }
+        const WV3 w = w_vertices(e, valid, x_prev, wRp, k0 + lane == h.klast, h.wInf_U);
+        int tot;
+        const int off = excl_prefix_sum(w.n, lane, tot);
+        if (nW + tot > wcap) return DEV_FALLBACK;  // cannot happen
+        for (int q = 0; q < w.n; ++q) {
+            const WV v = w.get(q);
+            Wb[nW + off + q] = Vtx{v.x, v.f, v.sR};
+        }
+        nW += tot;
+        const unsigned bu = __ballot_sync(FULLM, valid && (code & 1));
+        const unsigned bv = __ballot_sync(FULLM, valid);
+        const int cU = __popc(bu), cD = __popc(bv) - cU;
+        cx = __shfl_sync(FULLM, e.x, 31);
+        cwr = __shfl_sync(FULLM, (int)wr, 31) != 0;
+        __syncwarp();
+        if (lane == 0) {
+            if (cU > 0) Wn.u[0] = Wn.u[cU];
+            if (cD > 0) Wn.d[0] = Wn.d[cD];
+        }
+        a += cU;
+        b += cD;
+        __syncwarp();
+    }
+    if (nW == 0) return DEV_FALLBACK;  // W is a line: not a heavy node (caller falls back)
+    const double slW = h.tailL_U ? U.sl : D.sl;
+    const int nb = (nW + 31) / 32;
+
+    // ---- sweep B: Mafter[b] = min of g over blocks > b ----
+    {
+        double Mc = INFINITY;
+        for (int blk = nb - 1; blk >= 0; --blk) {
+            const int j = blk * 32 + lane;
+            double g = INFINITY;
+            if (j < nW) { const Vtx v = Wb[j]; g = fma(-lo, v.x, v.f); }
+            if (lane == 0) Mafter[blk] = Mc;
+            Mc = fmin(Mc, warp_min(g));
+        }
+    }
+    __syncwarp();
+
+    // ---- sweep C: z on every piece of W ----
+    const PCtx c{lo, hi, ux, uf, seller};
+    const int base = 0;
+    int total = 0;
+    int err = DEV_OK;
+    double Pc = INFINITY;
+    double s_in = lo;           // z's slope arriving from the left (z's left tail is lo)
+    double last_x = -INFINITY;  // the last vertex written (earlier blocks)
+    for (int blk = 0; blk < nb; ++blk) {
+        const int j = blk * 32 + lane;
+        const bool has = j < nW;
+        Vtx wv = has ? Wb[j] : Vtx{INFINITY, 0.0, 0.0};
+        double sL = __shfl_up_sync(FULLM, wv.s, 1);
+        if (lane == 0) sL = blk == 0 ? slW : Wb[j - 1].s;
+        double xn = __shfl_down_sync(FULLM, wv.x, 1);
+        if (lane == 31) xn = (j + 1 < nW) ? Wb[j + 1].x : INFINITY;
+        const double gl = has ? fma(-lo, wv.x, wv.f) : INFINITY;
+        const double hl = has ? fma(-hi, wv.x, wv.f) : INFINITY;
+        const double Mnext = fmin(excl_suffix_min(gl, lane), Mafter[blk]);  // g over later W vertices
+        const double Pl = fmin(excl_prefix_min(hl, lane), Pc);             // h over earlier W vertices
+        const bool first_overall = has && j == 0;
+        Stage st;
+        st.buf = stage_buf;
+        st.lane = lane;
+        st.m = 0;
+        st.err = DEV_OK;
+        st.last_s = NAN;
+        double s_run = NAN;
+        bool pending = false;
+        if (has) {
+            const double Mj = fmin(gl, Mnext);
+            if (first_overall) {
+                const Line LW{wv.x, wv.f, sL}, LM{0.0, Mj, lo}, LP{0.0, INFINITY, hi};
+                const double mv = LM.at(ux);
+                const double tl = ftol(mv, uf);
+                const bool zU0 = fabs(uf - mv) > tl ? (seller ? uf > mv : uf < mv) : false;
+                s_run = emit_open(-INFINITY, wv.x, LW, LM, true, LP, false, c, lo, zU0, st);
+            }
+            int vi;
+            bool zU;
+            double zv;
+            const double Pj = fmin(Pl, hl);
+            const Line LWr{wv.x, wv.f, wv.s}, LMr{0.0, Mnext, lo}, LPr{0.0, Pj, hi};
+            const double sr_ = z_side(LWr, LMr, isfinite(Mnext), LPr, true, c, wv.x, true, vi, zU, zv);
+            if (s_run != s_run) {
+                pending = st.m == 0;
+                st.push(wv.x, zv, sr_);
+            } else if (sr_ != s_run) {
+                st.push(wv.x, zv, sr_);
+            }
+            s_run = emit_open(wv.x, xn, LWr, LMr, isfinite(Mnext), LPr, true, c, sr_, false, st);
+        }
+        const double s_end = s_run;
+        // the slope arriving from the left: s_end of the previous lane (all lanes
+        // below the last valid one hold a vertex), or of the previous block
+        double s_left = __shfl_up_sync(FULLM, s_end, 1);
+        if (lane == 0) s_left = s_in;
+        {
+            const int lastv = min(31, nW - 1 - blk * 32);
+            s_in = __shfl_sync(FULLM, s_end, lastv);
+        }
+        const int skip0 = (pending && stage_buf[lane].s == s_left) ? 1 : 0;
+        if (__reduce_or_sync(FULLM, st.err)) { err = DEV_FALLBACK; break; }  // stage overflow
+        int cnt = st.m - skip0;
+        double f0x = 0.0, fs = 0.0, lx = -INFINITY;
+        if (cnt > 0) {
+            f0x = stage_buf[skip0 * 32 + lane].x;
+            fs = stage_buf[skip0 * 32 + lane].s;
+            lx = stage_buf[(st.m - 1) * 32 + lane].x;
+        }
+        int prevl = cnt > 0 ? lane : -1;
+        int nextl = cnt > 0 ? lane : 32;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULLM, prevl, o);
+            if (lane >= o) prevl = max(prevl, y);
+            const int z = __shfl_down_sync(FULLM, nextl, o);
+            if (lane + o < 32) nextl = min(nextl, z);
+        }
+        int pl = __shfl_up_sync(FULLM, prevl, 1);
+        if (lane == 0) pl = -1;
+        int nl = __shfl_down_sync(FULLM, nextl, 1);
+        if (lane == 31) nl = 32;
+        const double px = __shfl_sync(FULLM, lx, pl < 0 ? 0 : pl);
+        const double prev_x = pl < 0 ? last_x : px;
+        const bool fold = cnt > 0 && !(f0x > prev_x + xtol(f0x));
+        const int nfold = __shfl_sync(FULLM, (int)fold, nl > 31 ? 0 : nl);
+        const double nfs = __shfl_sync(FULLM, fs, nl > 31 ? 0 : nl);
+        if (cnt > 0 && nl <= 31 && nfold) stage_buf[(st.m - 1) * 32 + lane].s = nfs;
+        if (fold && pl < 0 && total > 0) arena[base + total - 1].s = fs;
+        const int drop_first = (fold && (pl >= 0 || total > 0)) ? 1 : 0;
+        cnt -= drop_first;
+        int tot;
+        const int off = excl_prefix_sum(cnt, lane, tot);
+        if (base + total + tot > acap) { err = DEV_OVERFLOW; break; }
+        for (int q = 0; q < cnt; ++q)
+            arena[base + total + off + q] = stage_buf[(q + skip0 + drop_first) * 32 + lane];
+        total += tot;
+        {
+            const int lastl = __shfl_sync(FULLM, prevl, 31);
+            const double lxl = __shfl_sync(FULLM, lx, lastl < 0 ? 0 : lastl);
+            if (lastl >= 0) last_x = lxl;
+        }
+        Pc = fmin(Pc, warp_min(hl));
+        __syncwarp();
+    }
+    if (err) return err;
+    if (total == 0) {
+        if (base + 1 > acap) return DEV_OVERFLOW;
+        if (lane == 0) arena[base] = Vtx{0.0, fma(lo, -ux, uf), lo};
+        total = 1;
+    }
+    __syncwarp();
     nZ = total;
     return DEV_OK;
 }

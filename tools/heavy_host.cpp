@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <string>
 #include "../paper_1110_2477_b200/csrc/pwl_lane.cuh"
 #include "../paper_1110_2477_b200/csrc/pwl_heavy.cuh"
 using namespace amtc;
@@ -24,6 +25,9 @@ int main(int argc, char** argv) {
     // every node is checked but the lane result is kept
     const int tl = argc > 1 ? std::atoi(argv[1]) : -1;
     const int verbose = argc > 2;
+    // HEAVY_VARIANT=lane: the lane-contiguous update; default: the block-synchronous one
+    const char* hv = std::getenv("HEAVY_VARIANT");
+    const bool block_variant = !(hv && std::string(hv) == "lane");
     double S0, K, K2, T, sg, R, k;
     int kind, N;
     while (std::scanf("%lf %lf %lf %lf %lf %lf %lf %d %d", &S0, &K, &K2, &T, &sg, &R, &k, &kind, &N) == 9) {
@@ -61,12 +65,18 @@ int main(int argc, char** argv) {
                     if (lane_node_update(U, D, lo, hi, ux, uf, seller, buf.data(), cap, 1, E)) { status = 1; break; }
                     std::vector<Vtx> zl(out.begin(), out.begin() + E.m);
                     // the warp path on the same children
-                    std::vector<Vtx> scratch(heavy::scratch_vertices(U.n + D.n) + 64), arena(8 * (U.n + D.n) + 64);
+                    std::vector<Vtx> scratch(heavy::scratch_vertices(U.n + D.n) + 4 * (U.n + D.n) + 64),
+                        arena(8 * (U.n + D.n) + 64);
                     int counter = 0, zoff = 0, nZ = 0, err = 0;
+                    heavy::HWin win;
                     warp_emu::run_warp([&](int lane) {
                         int zo, zn;
-                        const int e = heavy::node_update(U, D, lo, hi, ux, uf, seller, scratch.data(), (int)scratch.size(),
-                                                         arena.data(), &counter, (int)arena.size(), zo, zn, lane);
+                        const int e = block_variant
+                            ? (zo = 0, heavy::node_update_block(U, D, lo, hi, ux, uf, seller, &win, scratch.data(),
+                                                                (int)scratch.size(), arena.data(), (int)arena.size(),
+                                                                zn, lane))
+                            : heavy::node_update(U, D, lo, hi, ux, uf, seller, scratch.data(), (int)scratch.size(),
+                                                 arena.data(), &counter, (int)arena.size(), zo, zn, lane);
                         if (lane == 0) { err = e; zoff = zo; nZ = zn; }
                     });
                     if (err) { status = 2; if (verbose) std::printf("heavy err %d at t=%d j=%d\n", err, t, j); break; }

@@ -86,3 +86,9 @@ inline bool __any_sync(unsigned, int v) {
     return r != 0;
 }
 inline void __syncwarp(unsigned = 0xffffffffu) { warp_emu::bar()->arrive_and_wait(); }
+inline unsigned __ballot_sync(unsigned, int v) {
+    unsigned r = 0;
+    for (int l = 0; l < 32; ++l) r |= (warp_emu::xchg(v != 0 ? 1 : 0, l) ? 1u : 0u) << l;
+    return r;
+}
+inline int __popc(unsigned v) { return __builtin_popcount(v); }
