@@ -119,6 +119,41 @@ int amtc_price_crr_batch(const amtc_batch_soa* d_in, int64_t n, int32_t N, doubl
 int amtc_price_crr_batch_host(const amtc_batch_soa* h_in, int64_t n, int32_t N, double* h_price,
                               void* cuda_stream);
 
+/*
+ * k = 0 CRR price of ONE large tree on the current device (config 5a, N up to
+ * 10^5 and beyond).  The level is swept in bands of 128
+ * levels over warp tiles with ghost columns (region-B dependency).
+ * Synchronous on cuda_stream.  *price (HOST pointer) receives V_0(0); NaN and a
+ * non-zero status on invalid input (as amtc_price_crr_batch's validation).
+ */
+int amtc_price_crr_tree(const amtc_params* params, int32_t N, const amtc_payoff* payoff, double* price,
+                        void* cuda_stream);
+
+/*
+ * NCCL communicator for amtc_price_tree_sharded.  Rank 0 calls
+ * amtc_comm_unique_id and shares the 128 bytes with every rank (e.g. over the
+ * torch.distributed store); each rank then calls amtc_comm_init on its own
+ * device.  The communicator is owned by the caller (amtc_comm_destroy).
+ */
+int amtc_comm_unique_id(unsigned char id[128]);
+int amtc_comm_init(const unsigned char id[128], int nranks, int rank, void** comm);
+int amtc_comm_destroy(void* comm);
+
+/*
+ * One tree sharded over the nranks GPUs of an amtc_comm_init communicator
+ * (SURVEY 8(e), config 5): every rank calls it with the same arguments.  Rank
+ * g owns columns [ceil(g w/n), ceil((g+1) w/n)) of the current level (w = t+1),
+ * re-split every band of 128 levels (the paper's per-round rebalancing,
+ * P:178); before each band the ranks exchange their window halos with
+ * ncclSend/ncclRecv (region-B dependency).  Every rank receives the
+ * quote in *out (HOST pointer).  k = 0 only for nranks > 1 (the transaction-
+ * cost tree is not sharded yet: AMTC_EINVAL); with nranks = 1 and k > 0 this
+ * is amtc_price_american_tc.  nccl_comm may be NULL when nranks = 1.
+ * Synchronous on cuda_stream.  Returns the status (also in out->status).
+ */
+int amtc_price_tree_sharded(const amtc_params* params, int32_t N, const amtc_payoff* payoff, double k,
+                            void* nccl_comm, int rank, int nranks, amtc_quote* out, void* cuda_stream);
+
 /* Human-readable name of a status code (static storage). */
 const char* amtc_strerror(int status);
 

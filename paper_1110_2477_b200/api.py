@@ -48,7 +48,9 @@ assert QUOTE_DTYPE.itemsize == C.sizeof(Quote) == 24
 
 EXPORTS = ["amtc_price_american_tc", "amtc_price_american_tc_batch", "amtc_price_american_tc_batch_host",
            "amtc_price_crr_batch", "amtc_price_crr_batch_host", "amtc_strerror", "amtc_last_error",
-           "amtc_launch_count", "amtc_tc_last_stats", "amtc_debug_set_heavy_threshold"]
+           "amtc_launch_count", "amtc_tc_last_stats", "amtc_debug_set_heavy_threshold",
+           "amtc_price_crr_tree", "amtc_comm_unique_id", "amtc_comm_init", "amtc_comm_destroy",
+           "amtc_price_tree_sharded"]
 
 _lib = None
 
@@ -76,6 +78,13 @@ def lib():
         L.amtc_launch_count.restype = C.c_int64
         L.amtc_tc_last_stats.restype = C.c_int
         L.amtc_tc_last_stats.argtypes = [C.POINTER(TcStats)]
+        L.amtc_price_crr_tree.argtypes = [C.POINTER(Params), C.c_int32, C.POINTER(Payoff),
+                                          C.POINTER(C.c_double), C.c_void_p]
+        L.amtc_comm_unique_id.argtypes = [C.c_char_p]
+        L.amtc_comm_init.argtypes = [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        L.amtc_comm_destroy.argtypes = [C.c_void_p]
+        L.amtc_price_tree_sharded.argtypes = [C.POINTER(Params), C.c_int32, C.POINTER(Payoff), C.c_double,
+                                              C.c_void_p, C.c_int, C.c_int, C.POINTER(Quote), C.c_void_p]
         L.amtc_debug_set_heavy_threshold.restype = None
         L.amtc_debug_set_heavy_threshold.argtypes = [C.c_int]
         _lib = L
@@ -213,3 +222,61 @@ def price_crr_batch_host(batch, N: int, stream=None) -> np.ndarray:
                                          _stream_handle(stream))
     _check(rc, allow_option_status=False)
     return out
+
+
+# ---------------------------------------------------------------------------
+# one large tree (config 5): single GPU and sharded over an NCCL communicator
+# ---------------------------------------------------------------------------
+
+def price_crr_tree(S0: float, K: float, T: float, sigma: float, R: float, N: int, kind: int = PUT,
+                   K2: float = 0.0, stream=None) -> float:
+    """k = 0 CRR price of one (large) tree on the current device."""
+    p = Params(S0, T, sigma, R)
+    y = Payoff(kind, 0, K, K2)
+    v = C.c_double()
+    rc = lib().amtc_price_crr_tree(C.byref(p), N, C.byref(y), C.byref(v), _stream_handle(stream))
+    if rc:
+        raise ValueError(f"amtc_price_crr_tree: {STATUS.get(rc, rc)}")
+    return v.value
+
+
+def comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    rc = lib().amtc_comm_unique_id(buf)
+    if rc:
+        raise RuntimeError(f"amtc_comm_unique_id: {STATUS.get(rc, rc)}")
+    return buf.raw
+
+
+def comm_init(uid: bytes, nranks: int, rank: int) -> C.c_void_p:
+    comm = C.c_void_p()
+    rc = lib().amtc_comm_init(C.create_string_buffer(uid, 128), nranks, rank, C.byref(comm))
+    if rc:
+        raise RuntimeError(f"amtc_comm_init: {STATUS.get(rc, rc)}")
+    return comm
+
+
+def comm_destroy(comm) -> None:
+    lib().amtc_comm_destroy(comm)
+
+
+def comm_from_torch_dist(pg=None):
+    """Create the library's NCCL communicator over the ranks of torch.distributed
+    (the unique id travels through a broadcast_object_list)."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(pg), dist.get_world_size(pg)
+    obj = [comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=pg)
+    return comm_init(obj[0], world, rank), rank, world
+
+
+def price_tree_sharded(S0: float, K: float, T: float, sigma: float, R: float, N: int, k: float = 0.0,
+                       kind: int = PUT, K2: float = 0.0, comm=None, rank: int = 0, nranks: int = 1,
+                       stream=None) -> dict:
+    """One tree sharded over the ranks of `comm` (every rank calls it)."""
+    p = Params(S0, T, sigma, R)
+    y = Payoff(kind, 0, K, K2)
+    q = Quote()
+    rc = lib().amtc_price_tree_sharded(C.byref(p), N, C.byref(y), k, comm, rank, nranks, C.byref(q),
+                                       _stream_handle(stream))
+    return {"ask": q.ask, "bid": q.bid, "status": q.status if rc == q.status else rc, "max_bp": q.max_bp}

@@ -9,12 +9,25 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libamtc.so")
-SOURCES = ["amtc_capi.cu", "amtc_prepare.cu", "amtc_strip.cu", "amtc_crr.cu"]
+SOURCES = ["amtc_capi.cu", "amtc_prepare.cu", "amtc_strip.cu", "amtc_crr.cu", "amtc_tree.cu"]
 HEADERS = ["amtc_internal.cuh", "amtc_option.cuh", "pwl_device.cuh", "pwl_lane.cuh", "pwl_heavy.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_dir() -> str:
+    """NCCL of the torch wheel (the same library torch.distributed loads)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec and spec.submodule_search_locations:
+        return list(spec.submodule_search_locations)[0]
+    return "/usr"
+
+
+NCCL = _nccl_dir()
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr",
-         "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+         "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", os.path.join(NCCL, "include")]
+LINK = ["-L", os.path.join(NCCL, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath," + os.path.join(NCCL, "lib")]
 
 
 def _stale() -> bool:
@@ -37,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         subprocess.run(cmd, check=True)
         objs.append(obj)
     tmp = LIB + ".tmp"
-    subprocess.run([NVCC, "-shared", *FLAGS, *objs, "-o", tmp, "-lcudart"], check=True)
+    subprocess.run([NVCC, "-shared", *FLAGS, *objs, "-o", tmp, "-lcudart", *LINK], check=True)
     os.replace(tmp, LIB)
     return LIB
 

@@ -1,0 +1,371 @@
+// amtc_tree.cu -- ONE large frictionless (k = 0) CRR tree (config 5a: N up to
+// 10^5 and beyond), on one GPU or sharded over the GPUs of an NCCL
+// communicator.
+//
+// Recursion (Appendix; no extra level in frictionless mode):
+//   V_N(j) = max(P(S_{N,j}), 0),  V_t(j) = max(P(S_{t,j}), p_u V_{t+1}(j) + p_d V_{t+1}(j+1)).
+// Node (t, j) needs (t+1, j) and (t+1, j+1): the dependency cone of a band of
+// D levels over output columns [j0, j0 + W) is the input window [j0, j0 + W + D)
+// at the band's top level (the paper's region-B dependency).
+//
+// Band kernel: each warp owns M = 16 consecutive columns per lane (512 columns,
+// the level in registers); it reads the 512-column window at level t_top,
+// runs D = 128 levels with one 64-bit shuffle per level (the j+1 neighbour of
+// a lane's last column), and writes the first 384 columns of level t_top - D
+// (the right 128 columns become invalid one per level: the ghost zone).  A
+// band is one launch; the level lives in HBM/L2 between bands (800 KB at
+// N = 10^5).  No shared memory, no __syncthreads: warps are independent.
+//
+// The exercise value is carried incrementally per column (S_{t,j} = d S_{t+1,j}):
+// put X = K - S: X_t = d X_{t+1} + K (1 - d); call X = S - K: X_t = d X_{t+1} - K (1 - d).
+// max(X, c) with c = p_u V + p_d V' >= +0 is a signed 64-bit integer max of the
+// bit patterns (IEEE order of non-negative doubles = integer order; a negative X
+// has a negative pattern), which runs on the integer ALU instead of the FP64
+// pipe's slow DMNMX (4.0e12/s vs 1.8e13/s DFMA on B200, profiles/r01_fp64_peak.json).
+//
+// Sharding (amtc_price_tree_sharded): rank g owns columns
+// [ceil(g w / n), ceil((g+1) w / n)) of the current level (w = t + 1 columns,
+// re-split every band -- the paper's per-round rebalancing).  Before a
+// band each rank gathers its input window from the owners (ncclSend/ncclRecv
+// in one group: its own range plus a halo of D columns from the right and the
+// re-split shift from the left), then runs the band kernel locally.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <mutex>
+#include <string>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "amtc.h"
+#include "amtc_internal.cuh"
+
+namespace amtc {
+
+constexpr int TREE_M = 16;                      // columns per lane
+constexpr int TREE_COLS = 32 * TREE_M;          // window columns per warp
+constexpr int TREE_D = 128;                     // levels per band
+constexpr int TREE_W = TREE_COLS - TREE_D;      // output columns per warp
+constexpr int TREE_THREADS = 128;
+
+struct TreeConsts {
+    double S0, K, K2, h, pu, pd, d, c0;
+    int kind;
+};
+
+__device__ __forceinline__ double max_nonneg(double x, double c) {  // max(x, c) for c >= +0
+    return __longlong_as_double(max(__double_as_longlong(x), __double_as_longlong(c)));
+}
+
+// exercise state of column j at level t: put/call X = +-(K - S); bull: X = S
+__device__ __forceinline__ double exercise_state(const TreeConsts& c, int t, int64_t j) {
+    const double S = c.S0 * exp(c.h * (double)((int64_t)t - 2 * j));
+    if (c.kind == KIND_PUT) return c.K - S;
+    if (c.kind == KIND_CALL) return S - c.K;
+    return S;
+}
+__device__ __forceinline__ double exercise_value(const TreeConsts& c, double X) {
+    if (c.kind == KIND_BULL) return fmin(fmax(X - c.K, 0.0), c.K2 - c.K);
+    return X;
+}
+
+// leaves: V_N(j) = max(P(S_{N,j}), 0) for j in [j0, j0 + n)
+__global__ void tree_leaves_kernel(TreeConsts c, int N, int64_t j0, int64_t n, double* v) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    v[i] = fmax(exercise_value(c, exercise_state(c, N, j0 + i)), 0.0);
+}
+
+// one band: levels t_top-1 .. t_top-D'; vin holds level t_top for columns
+// [jin0, jin0 + nin); vout receives level t_top - D' for [jout0, jout0 + nout)
+template <int KIND>
+__global__ void __launch_bounds__(TREE_THREADS) tree_band_kernel(TreeConsts c, int t_top, int Dp,
+                                                                 const double* __restrict__ vin, int64_t jin0,
+                                                                 int64_t nin, double* __restrict__ vout,
+                                                                 int64_t jout0, int64_t nout) {
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t jw = jout0 + w * TREE_W;
+    if (jw >= jout0 + nout) return;  // warp-uniform
+    double V[TREE_M], X[TREE_M];
+#pragma unroll
+    for (int q = 0; q < TREE_M; ++q) {
+        const int64_t j = jw + lane * TREE_M + q;
+        const int64_t i = j - jin0;
+        V[q] = (i < nin) ? vin[i] : 0.0;  // beyond the window: ghost columns, never read back
+        X[q] = exercise_state(c, t_top, j);
+    }
+    for (int l = 0; l < Dp; ++l) {
+        const double nb = __shfl_down_sync(0xffffffffu, V[0], 1);
+#pragma unroll
+        for (int q = 0; q < TREE_M; ++q) {
+            const double vn = (q + 1 < TREE_M) ? V[q + 1] : nb;
+            double ex;
+            if (KIND == KIND_BULL) {
+                X[q] *= c.d;
+                ex = fmin(fmax(X[q] - c.K, 0.0), c.K2 - c.K);
+            } else {
+                X[q] = fma(c.d, X[q], c.c0);
+                ex = X[q];
+            }
+            V[q] = max_nonneg(ex, fma(c.pu, V[q], c.pd * vn));
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < TREE_M; ++q) {
+        const int64_t off = (int64_t)lane * TREE_M + q;
+        const int64_t j = jw + off;
+        if (off < TREE_W && j < jout0 + nout) vout[j - jout0] = V[q];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static int tree_consts(const amtc_params* p, int N, const amtc_payoff* pay, TreeConsts& c) {
+    if (!p || !pay || pay->flags != 0 || N < 1) return STATUS_EINVAL;
+    if (!(p->S0 > 0.0) || !(p->T > 0.0) || !(p->sigma > 0.0) || !std::isfinite(p->R)) return STATUS_EINVAL;
+    c.kind = pay->kind;
+    c.S0 = p->S0;
+    c.K = pay->K;
+    c.K2 = pay->K2;
+    if (c.kind != KIND_PUT && c.kind != KIND_CALL && c.kind != KIND_BULL) return STATUS_EINVAL;
+    if (c.kind != KIND_BULL && !(c.K > 0.0)) return STATUS_EINVAL;
+    if (c.kind == KIND_BULL && !(c.K < c.K2)) return STATUS_EINVAL;
+    c.h = p->sigma * std::sqrt(p->T / (double)N);
+    const double rho = p->R * p->T / (double)N;
+    if (!(rho < c.h && -c.h < rho)) return STATUS_EARBITRAGE;  // d < r < u
+    const double u = std::exp(c.h), r = std::exp(rho);
+    c.d = 1.0 / u;
+    const double pr = (r - c.d) / (u - c.d);  // risk-neutral probability
+    c.pu = pr / r;
+    c.pd = (1.0 - pr) / r;
+    c.c0 = (c.kind == KIND_PUT) ? c.K * (1.0 - c.d) : -c.K * (1.0 - c.d);
+    return STATUS_OK;
+}
+
+static void launch_leaves(const TreeConsts& c, int N, int64_t j0, int64_t n, double* v, cudaStream_t s) {
+    if (n <= 0) return;
+    tree_leaves_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c, N, j0, n, v);
+    note_launch();
+}
+
+static void launch_band(const TreeConsts& c, int t_top, int Dp, const double* vin, int64_t jin0, int64_t nin,
+                        double* vout, int64_t jout0, int64_t nout, cudaStream_t s) {
+    if (nout <= 0) return;
+    const int64_t warps = (nout + TREE_W - 1) / TREE_W;
+    const unsigned blocks = (unsigned)((warps * 32 + TREE_THREADS - 1) / TREE_THREADS);
+    if (c.kind == KIND_PUT)
+        tree_band_kernel<KIND_PUT><<<blocks, TREE_THREADS, 0, s>>>(c, t_top, Dp, vin, jin0, nin, vout, jout0, nout);
+    else if (c.kind == KIND_CALL)
+        tree_band_kernel<KIND_CALL><<<blocks, TREE_THREADS, 0, s>>>(c, t_top, Dp, vin, jin0, nin, vout, jout0, nout);
+    else
+        tree_band_kernel<KIND_BULL><<<blocks, TREE_THREADS, 0, s>>>(c, t_top, Dp, vin, jin0, nin, vout, jout0, nout);
+    note_launch();
+}
+
+// grow-only device buffers of this translation unit (per device, mutex-guarded)
+struct TreeBufs {
+    std::mutex mu;
+    double* p[3] = {nullptr, nullptr, nullptr};
+    size_t n = 0;
+    double* h_pinned = nullptr;
+    cudaError_t ensure(size_t want) {
+        if (want <= n) return cudaSuccess;
+        for (auto& q : p) {
+            if (q) cudaFree(q);
+            q = nullptr;
+        }
+        n = 0;
+        for (auto& q : p) {
+            cudaError_t e = cudaMalloc(&q, want * sizeof(double));
+            if (e != cudaSuccess) return e;
+        }
+        if (!h_pinned) {
+            cudaError_t e = cudaMallocHost(&h_pinned, sizeof(double));
+            if (e != cudaSuccess) return e;
+        }
+        n = want;
+        return cudaSuccess;
+    }
+};
+static TreeBufs* tree_bufs() {
+    static std::mutex mu;
+    static std::vector<TreeBufs*> v;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    if ((int)v.size() <= dev) v.resize(dev + 1, nullptr);
+    if (!v[dev]) v[dev] = new TreeBufs();
+    return v[dev];
+}
+
+// rank g's columns of a level of width w over n ranks: [a_g, a_{g+1}),
+// a_g = ceil(g w / n) (rank 0 keeps the root column)
+static inline int64_t split_at(int64_t w, int g, int n) { return (g * w + n - 1) / n; }
+
+static thread_local std::string t_err;
+static int cuda_err(cudaError_t e, const char* what) {
+    t_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return STATUS_ECUDA;
+}
+
+// the whole tree, ranks 0..n-1 of comm (comm == nullptr: one GPU, no NCCL)
+static int tree_run(const TreeConsts& c, int N, ncclComm_t comm, int rank, int nranks, double* price,
+                    cudaStream_t s) {
+    TreeBufs* B = tree_bufs();
+    std::lock_guard<std::mutex> guard(B->mu);
+    const int64_t cap = (N + 1 + nranks - 1) / nranks + TREE_D + 64;
+    cudaError_t e = B->ensure((size_t)cap);
+    if (e != cudaSuccess) return cuda_err(e, "tree buffers");
+    double* cur = B->p[0];   // own columns of the current level
+    double* win = B->p[1];   // input window of the band
+    double* nxt = B->p[2];   // own columns of the next level
+    // leaves (t = N), own range
+    int64_t a = split_at(N + 1, rank, nranks), b = split_at(N + 1, rank + 1, nranks);
+    launch_leaves(c, N, a, b - a, cur, s);
+    for (int t_top = N; t_top > 0;) {
+        const int Dp = std::min(TREE_D, t_top);
+        const int t_bot = t_top - Dp;
+        const int64_t w1 = t_top + 1, w0 = t_bot + 1;
+        // every rank's window [lo, hi) at t_top (empty if it owns nothing at t_bot)
+        auto need = [&](int g, int64_t& lo, int64_t& hi) {
+            const int64_t a0 = split_at(w0, g, nranks), b0 = split_at(w0, g + 1, nranks);
+            lo = a0;
+            hi = (b0 > a0) ? std::min(b0 + Dp, w1) : a0;
+        };
+        int64_t my_lo, my_hi;
+        need(rank, my_lo, my_hi);
+        // gather the window: intersections of owners' ranges with windows
+        if (comm) {
+            if (ncclGroupStart() != ncclSuccess) return STATUS_ENCCL;
+        }
+        for (int h = 0; h < nranks; ++h) {
+            const int64_t ha = split_at(w1, h, nranks), hb = split_at(w1, h + 1, nranks);
+            if (h == rank) {
+                // sends of my range to the others' windows
+                for (int g = 0; g < nranks; ++g) {
+                    if (g == rank) continue;
+                    int64_t lo, hi;
+                    need(g, lo, hi);
+                    const int64_t x0 = std::max(lo, ha), x1 = std::min(hi, hb);
+                    if (x1 > x0 && ncclSend(cur + (x0 - ha), (size_t)(x1 - x0), ncclDouble, g, comm, s) != ncclSuccess)
+                        return STATUS_ENCCL;
+                }
+            } else {
+                const int64_t x0 = std::max(my_lo, ha), x1 = std::min(my_hi, hb);
+                if (x1 > x0 && ncclRecv(win + (x0 - my_lo), (size_t)(x1 - x0), ncclDouble, h, comm, s) != ncclSuccess)
+                    return STATUS_ENCCL;
+            }
+        }
+        if (comm) {
+            if (ncclGroupEnd() != ncclSuccess) return STATUS_ENCCL;
+        }
+        {
+            const int64_t x0 = std::max(my_lo, a), x1 = std::min(my_hi, b);
+            if (x1 > x0) {
+                e = cudaMemcpyAsync(win + (x0 - my_lo), cur + (x0 - a), sizeof(double) * (x1 - x0),
+                                    cudaMemcpyDeviceToDevice, s);
+                if (e != cudaSuccess) return cuda_err(e, "window copy");
+            }
+        }
+        const int64_t a0 = split_at(w0, rank, nranks), b0 = split_at(w0, rank + 1, nranks);
+        launch_band(c, t_top, Dp, win, my_lo, my_hi - my_lo, nxt, a0, b0 - a0, s);
+        std::swap(cur, nxt);
+        a = a0;
+        b = b0;
+        t_top = t_bot;
+    }
+    // the root column belongs to rank 0; share it
+    if (comm) {
+        if (ncclBroadcast(cur, cur, 1, ncclDouble, 0, comm, s) != ncclSuccess) return STATUS_ENCCL;
+    }
+    e = cudaMemcpyAsync(B->h_pinned, cur, sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_err(e, "root copy");
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_err(e, "tree sync");
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_err(e, "tree kernels");
+    *price = *B->h_pinned;
+    return STATUS_OK;
+}
+
+}  // namespace amtc
+
+using namespace amtc;
+
+extern "C" {
+
+int amtc_price_crr_tree(const amtc_params* params, int32_t N, const amtc_payoff* payoff, double* price,
+                        void* cuda_stream) {
+    try {
+        if (!price) return STATUS_EINVAL;
+        *price = NAN;
+        TreeConsts c;
+        const int st = tree_consts(params, N, payoff, c);
+        if (st) return st;
+        return tree_run(c, N, nullptr, 0, 1, price, static_cast<cudaStream_t>(cuda_stream));
+    } catch (...) {
+        return STATUS_ECUDA;
+    }
+}
+
+int amtc_comm_unique_id(unsigned char id[128]) {
+    ncclUniqueId u;
+    if (ncclGetUniqueId(&u) != ncclSuccess) return STATUS_ENCCL;
+    static_assert(sizeof(u.internal) == 128, "ncclUniqueId size");
+    for (int i = 0; i < 128; ++i) id[i] = (unsigned char)u.internal[i];
+    return STATUS_OK;
+}
+
+int amtc_comm_init(const unsigned char id[128], int nranks, int rank, void** comm_out) {
+    if (!id || !comm_out || nranks < 1 || rank < 0 || rank >= nranks) return STATUS_EINVAL;
+    ncclUniqueId u;
+    for (int i = 0; i < 128; ++i) u.internal[i] = (char)id[i];
+    ncclComm_t comm;
+    if (ncclCommInitRank(&comm, nranks, u, rank) != ncclSuccess) return STATUS_ENCCL;
+    *comm_out = comm;
+    return STATUS_OK;
+}
+
+int amtc_comm_destroy(void* comm) {
+    if (!comm) return STATUS_EINVAL;
+    return ncclCommDestroy(static_cast<ncclComm_t>(comm)) == ncclSuccess ? STATUS_OK : STATUS_ENCCL;
+}
+
+int amtc_price_tree_sharded(const amtc_params* params, int32_t N, const amtc_payoff* payoff, double k,
+                            void* nccl_comm, int rank, int nranks, amtc_quote* out, void* cuda_stream) {
+    try {
+        if (!out) return STATUS_EINVAL;
+        out->ask = out->bid = NAN;
+        out->max_bp = 0;
+        out->status = STATUS_EINVAL;
+        if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !nccl_comm)) return STATUS_EINVAL;
+        if (!(k >= 0.0 && k < 1.0)) return STATUS_EINVAL;
+        if (k > 0.0) {
+            // the transaction-cost tree is not sharded yet: one GPU only
+            if (nranks != 1) return STATUS_EINVAL;
+            *out = amtc_price_american_tc(params, N, payoff, k);
+            return out->status;
+        }
+        TreeConsts c;
+        int st = tree_consts(params, N, payoff, c);
+        if (st) { out->status = st; return st; }
+        double price = NAN;
+        st = tree_run(c, N, static_cast<ncclComm_t>(nccl_comm), rank, nranks, &price,
+                      static_cast<cudaStream_t>(cuda_stream));
+        out->status = st;
+        if (!st) {
+            out->ask = price;  // k = 0: ask = bid = the CRR price (derived A.1)
+            out->bid = price;
+            out->max_bp = 1;
+        }
+        return st;
+    } catch (...) {
+        return STATUS_ECUDA;
+    }
+}
+
+}  // extern "C"

@@ -20,6 +20,9 @@
 // slope arriving from the left, and compacted with a warp prefix sum.
 #pragma once
 #include "pwl_device.cuh"
+#ifdef HEAVY_STATS
+extern long g_stat[8];
+#endif
 
 namespace amtc {
 namespace heavy {
@@ -1077,13 +1080,35 @@ __device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo,
             const double Pj = fmin(Pl, hl);
             const Line LWr{wv.x, wv.f, wv.s}, LMr{0.0, Mnext, lo}, LPr{0.0, Pj, hi};
             const double sr_ = z_side(LWr, LMr, isfinite(Mnext), LPr, true, c, wv.x, true, vi, zU, zv);
+#ifdef HEAVY_STATS
+            {
+                
+                const int m0 = st.m;
+                const double sr2 = sr_;
+                (void)sr2;
+                g_stat[0]++;
+                if (wv.s >= lo && wv.s <= hi) g_stat[1]++;
+                if (vi == 0 && !zU) g_stat[2]++;
+                (void)m0;
+            }
+#endif
             if (s_run != s_run) {
                 pending = st.m == 0;
                 st.push(wv.x, zv, sr_);
             } else if (sr_ != s_run) {
                 st.push(wv.x, zv, sr_);
             }
+#ifdef HEAVY_STATS
+            const int m1 = st.m;
+#endif
             s_run = emit_open(wv.x, xn, LWr, LMr, isfinite(Mnext), LPr, true, c, sr_, false, st);
+#ifdef HEAVY_STATS
+            {
+                
+                if (st.m == m1) g_stat[3]++;
+                if (st.m == m1 && vi == 0 && !zU) g_stat[4]++;
+            }
+#endif
         }
         const double s_end = s_run;
         // the slope arriving from the left: s_end of the previous lane (all lanes

@@ -1,0 +1,94 @@
+"""GPU parity of the single large-tree path (config 5a) and of the sharded
+entry point on one rank, through the C-ABI, against the CPU oracle."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1110_2477_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+RTOL, ATOL = 1e-9, 1e-12 * 100.0  # north star + reading A19 floor (S0 = 100)
+
+
+@pytest.fixture(scope="module")
+def api():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_1110_2477_b200 import api as A
+    A.lib()
+    return A
+
+
+def _close(g, o):
+    return abs(g - o) <= RTOL * abs(o) + ATOL
+
+
+CASES = [(O.PUT, 100.0, 0.0), (O.CALL, 95.0, 0.0), (O.BULL, 90.0, 110.0)]
+
+
+# band edges: 128 levels per band, 384 output columns per warp
+@pytest.mark.parametrize("N", [1, 2, 127, 128, 129, 383, 384, 385, 511, 1000, 5001])
+@pytest.mark.parametrize("case", range(3))
+def test_crr_tree_matches_oracle(api, N, case):
+    kind, K, K2 = CASES[case]
+    g = api.price_crr_tree(100.0, K, 0.8, 0.3, 0.04, N, kind, K2)
+    o = O.price_crr(O.Option(100.0, K, 0.8, 0.3, 0.04, 0.0, kind, K2), N)
+    assert _close(g, o), (N, kind, g, o)
+
+
+def test_crr_tree_equals_batch_kernel(api):
+    b = W.random_small(16, seed=77, k_max=0.0)
+    N = 700
+    batch = api.price_crr_batch_host(b, N)
+    for i in range(len(b)):
+        r = b.row(i)
+        g = api.price_crr_tree(r["S0"], r["K"], r["T"], r["sigma"], r["R"], N, r["kind"], r["K2"])
+        assert _close(g, batch[i]), (i, g, batch[i])
+
+
+def test_appendix_put_13906(api):
+    """American put K=S0=100, T=3, sigma=0.3, R=0.06 -> 13.906 (reading A16: N=40000)."""
+    a = W.appendix_put().row(0)
+    g = api.price_crr_tree(a["S0"], a["K"], a["T"], a["sigma"], a["R"], 40000, O.PUT)
+    assert abs(g - 13.906) <= 5e-4
+    o = O.price_crr(O.Option(a["S0"], a["K"], a["T"], a["sigma"], a["R"], 0.0, O.PUT), 40000)
+    assert _close(g, o), (g, o)
+
+
+def test_config5a_full_size(api):
+    """BASELINE config 5a: put S0=K=100, T=1, sigma=0.3, R=0.05, k=0, N=100000."""
+    r = W.config5a().row(0)
+    g = api.price_crr_tree(r["S0"], r["K"], r["T"], r["sigma"], r["R"], W.CONFIG5A_N, O.PUT)
+    o = O.price_crr(O.Option(r["S0"], r["K"], r["T"], r["sigma"], r["R"], 0.0, O.PUT), W.CONFIG5A_N)
+    assert _close(g, o), (g, o)
+
+
+def test_tree_invalid_inputs(api):
+    with pytest.raises(ValueError):
+        api.price_crr_tree(-1.0, 100.0, 1.0, 0.2, 0.05, 100)
+    with pytest.raises(ValueError):  # d < r < u violated
+        api.price_crr_tree(100.0, 100.0, 1.0, 0.01, 5.0, 10)
+
+
+def test_sharded_one_rank_nccl(api):
+    """amtc_price_tree_sharded over a one-rank NCCL communicator: the same
+    numbers as the single-GPU tree (k = 0) and the single-option TC call (k > 0)."""
+    comm = api.comm_init(api.comm_unique_id(), 1, 0)
+    try:
+        for N in (130, 2000):
+            q = api.price_tree_sharded(100.0, 100.0, 1.0, 0.3, 0.05, N, 0.0, O.PUT, comm=comm, rank=0, nranks=1)
+            o = O.price_crr(O.Option(100.0, 100.0, 1.0, 0.3, 0.05, 0.0, O.PUT), N)
+            assert q["status"] == 0 and _close(q["ask"], o) and q["bid"] == q["ask"], (q, o)
+        q = api.price_tree_sharded(100.0, 100.0, 1.0, 0.3, 0.05, 200, 0.005, O.PUT, comm=comm, rank=0, nranks=1)
+        o = O.price_tc(O.Option(100.0, 100.0, 1.0, 0.3, 0.05, 0.005, O.PUT), 200)
+        assert q["status"] == 0 and _close(q["ask"], o.ask) and _close(q["bid"], o.bid), (q, o)
+    finally:
+        api.comm_destroy(comm)
+    # no communicator, one rank
+    q = api.price_tree_sharded(100.0, 100.0, 1.0, 0.3, 0.05, 300, 0.0, O.PUT)
+    assert q["status"] == 0
+    # k > 0 cannot be sharded yet
+    q = api.price_tree_sharded(100.0, 100.0, 1.0, 0.3, 0.05, 300, 0.005, O.PUT, comm=None, rank=0, nranks=2)
+    assert q["status"] == 1 and math.isnan(q["ask"])
