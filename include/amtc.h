@@ -182,6 +182,12 @@ int amtc_tc_last_stats(amtc_tc_stats* out);
    against the oracle.  tl <= 0 restores the default.  Affects later calls. */
 void amtc_debug_set_heavy_threshold(int tl);
 
+/* TESTING HOOK: strip-split mode of the transaction-cost solver (the strips
+   of one tree on different warps, pipelined through progress counters):
+   -1 automatic (default: when the batch has fewer items than a quarter of
+   the resident warps), 0 never, 1 whenever it fits in memory. */
+void amtc_debug_set_split_mode(int mode);
+
 #ifdef __cplusplus
 }
 #endif

@@ -55,6 +55,7 @@ struct DevBuf {
 struct DevState {
     std::mutex mu;
     DevBuf items[2], cls, small, ws, stage_in, stage_out;
+    DevBuf sp_items, sp_progress, sp_carry, sp_arena, sp_cnt;  // split mode
     int sm_count = 0;
     int occupancy = 0;
     // stats of the last TC batch
@@ -86,7 +87,10 @@ static bool soa_ok(const amtc_batch_soa* b) {
 }
 
 // small device scratch layout (ints)
-enum { SM_HIST = 0, SM_WORK = TC_CLASSES + 1, SM_OVF0, SM_OVF1, SM_WORST, SM_VSUM = 32, SM_INTS = 64 };
+enum { SM_HIST = 0, SM_WORK = TC_CLASSES + 1, SM_OVF0, SM_OVF1, SM_WORST, SM_SPLITN, SM_VSUM = 32, SM_INTS = 64 };
+
+// split mode policy (testing hook amtc_debug_set_split_mode): -1 auto, 0 off, 1 on when it fits
+static int g_split_mode = -1;
 
 // solver passes: every item first runs at capacity level 0; items that
 // overflowed a capacity (arena, scratch) are re-run at the next level (4x the
@@ -137,6 +141,79 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
     if (!st->ev[0]) {
         for (auto& e : st->ev) AMTC_CUDA(cudaEventCreate(&e));
     }
+    st->retried = 0;
+
+    // Split mode: with few trees (fewer items than a quarter of the resident
+    // warps) the strips of each tree run on different warps, pipelined through
+    // per-strip progress counters (intra-tree parallelism: configs 1, 3, 5b).
+    {
+        const int S = N / 32 + 1;
+        const int64_t warps_total = (int64_t)st->sm_count * st->occupancy * wpc;
+        const int64_t nsp = n2 * S;
+        bool want = (g_split_mode == 1 || (g_split_mode < 0 && n2 <= warps_total / 4)) && N >= 64 &&
+                    nsp < ((int64_t)1 << 30);
+        const size_t carry_b = strip_carry_bytes(N);
+        const int acap = strip_split_arena_cap(N);
+        const size_t need_b = (size_t)nsp * (carry_b + 2 * sizeof(int)) + (size_t)n2 * acap * strip_vtx_bytes();
+        if (want && need_b > budget / 2) want = false;
+        if (want) {
+            const size_t wsb = strip_ws_bytes_per_warp(N, 0);
+            int64_t ctas = std::min<int64_t>((int64_t)st->sm_count * st->occupancy, (nsp + wpc - 1) / wpc);
+            ctas = std::min<int64_t>(ctas, (int64_t)((budget - need_b) / (wsb * wpc)));
+            if (ctas < 1) want = false;
+            if (want) {
+                AMTC_CUDA(st->ws.ensure(wsb * wpc * (size_t)ctas));
+                AMTC_CUDA(st->sp_items.ensure(sizeof(int) * (size_t)nsp));
+                AMTC_CUDA(st->sp_progress.ensure(sizeof(int) * (size_t)nsp));
+                AMTC_CUDA(st->sp_carry.ensure(carry_b * (size_t)nsp));
+                AMTC_CUDA(st->sp_arena.ensure((size_t)n2 * acap * strip_vtx_bytes()));
+                AMTC_CUDA(st->sp_cnt.ensure(sizeof(int) * (size_t)n2));
+                AMTC_CUDA(cudaMemsetAsync(st->sp_progress.p, 0x7f, sizeof(int) * (size_t)nsp, s));
+                AMTC_CUDA(cudaMemsetAsync(st->sp_cnt.p, 0, sizeof(int) * (size_t)n2, s));
+                tc_launch_split_expand(q_items, q_count, S, nsp, static_cast<int*>(st->sp_items.p), small + SM_SPLITN,
+                                       s);
+                AMTC_CUDA(cudaMemsetAsync(small + SM_WORK, 0, sizeof(int), s));
+                AMTC_CUDA(cudaMemsetAsync(small + SM_OVF0, 0, sizeof(int), s));
+                AMTC_CUDA(cudaEventRecord(st->ev[0], s));
+                StripLaunchArgs A;
+                A.in = in;
+                A.N = N;
+                A.out = out;
+                A.items = static_cast<int*>(st->sp_items.p);
+                A.n_items = small + SM_SPLITN;
+                A.work_counter = small + SM_WORK;
+                A.ovf_items = static_cast<int*>(st->items[1].p);
+                A.ovf_count = small + SM_OVF0;
+                A.vertex_sum = reinterpret_cast<unsigned long long*>(small + SM_VSUM);
+                A.ws = static_cast<char*>(st->ws.p);
+                A.ws_stride = wsb;
+                A.level = 0;
+                A.ctas = (int)ctas;
+                A.split_S = S;
+                A.progress = static_cast<int*>(st->sp_progress.p);
+                A.carry = static_cast<char*>(st->sp_carry.p);
+                A.carry_stride = carry_b;
+                A.carena_split = st->sp_arena.p;
+                A.carena_cnt = static_cast<int*>(st->sp_cnt.p);
+                A.carena_split_cap = acap;
+                if (strip_launch(A, s) != STATUS_OK) return cuda_fail(cudaGetLastError(), "strip_kernel launch");
+                AMTC_CUDA(cudaEventRecord(st->ev[1], s));
+                passes = 1;
+                AMTC_CUDA(cudaMemcpyAsync(&ovf_host, small + SM_OVF0, sizeof(int), cudaMemcpyDeviceToHost, s));
+                AMTC_CUDA(cudaStreamSynchronize(s));
+                if (ovf_host > 0) {
+                    // a strip outgrew the split-mode capacities: redo every tree in whole-tree mode
+                    st->retried = ovf_host;
+                    tc_launch_prepare(in, n, N, out, static_cast<unsigned char*>(st->cls.p), small + SM_HIST,
+                                      static_cast<int*>(st->items[0].p), s);
+                    AMTC_CUDA(cudaMemsetAsync(small + SM_VSUM, 0, sizeof(unsigned long long), s));
+                    ovf_host = 0;
+                } else {
+                    goto finish;
+                }
+            }
+        }
+    }
     for (int level = 0; level <= kMaxLevel; ++level) {
         const size_t wsb = strip_ws_bytes_per_warp(N, level);
         int64_t ctas = (int64_t)st->sm_count * st->occupancy;
@@ -169,13 +246,15 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
         passes++;
         AMTC_CUDA(cudaMemcpyAsync(&ovf_host, ovf_count, sizeof(int), cudaMemcpyDeviceToHost, s));
         AMTC_CUDA(cudaStreamSynchronize(s));
-        if (passes == 1) st->retried = ovf_host;
+        if (level == 0) st->retried += ovf_host;
         if (ovf_host == 0) break;
         q_items = ovf_items;
         q_count = ovf_count;
         queued = ovf_host;
+        if (passes >= 8) break;  // event slots
     }
     if (ovf_host > 0) tc_launch_mark_capacity(q_items, ovf_host, out, s);
+finish:
     launch_status_reduce(out, n, small + SM_WORST, s);
     int worst = 0;
     unsigned long long vs = 0;
@@ -339,6 +418,8 @@ const char* amtc_strerror(int status) {
 const char* amtc_last_error(void) { return g_last_error.c_str(); }
 
 void amtc_debug_set_heavy_threshold(int tl) { strip_set_heavy_threshold(tl); }
+
+void amtc_debug_set_split_mode(int mode) { g_split_mode = mode < 0 ? -1 : (mode ? 1 : 0); }
 
 int64_t amtc_launch_count(void) { return g_launches.load(); }
 

@@ -16,7 +16,7 @@
 // The exercise value is carried incrementally: S_{t,j} = d S_{t+1,j}, so for
 // the put X = K - S obeys X_t = d X_{t+1} + K(1-d) (one DFMA), for the call
 // X_t = d X_{t+1} - K(1-d); the bull spread keeps S and clamps.
-// FP64 per node-update: DFMA (X) + DMUL + DFMA (continuation) + DMNMX.
+// FP64 per node-update: DFMA (X) + DMUL + DFMA (continuation); the max runs on the integer ALU.
 #include <cuda_runtime.h>
 
 #include "amtc_internal.cuh"
@@ -24,6 +24,19 @@
 namespace amtc {
 
 constexpr int CRR_M = 4;
+
+// max(x, c) for c >= +0 and min(a, b) for a, b >= +0 as signed 64-bit integer
+// max / min of the bit patterns (IEEE order of non-negative doubles is the
+// integer order; a negative x has a negative pattern): integer-ALU work instead
+// of the FP64 pipe's DMNMX, which issues at 1/4.5 of the DFMA rate on B200
+// (profiles/r01_fp64_peak.json).  Every V is >= +0 (max with a continuation
+// value p_u V + p_d V' of non-negative values).
+__device__ __forceinline__ double max_nonneg(double x, double c) {
+    return __longlong_as_double(max(__double_as_longlong(x), __double_as_longlong(c)));
+}
+__device__ __forceinline__ double min_nonneg(double a, double b) {
+    return __longlong_as_double(min(__double_as_longlong(a), __double_as_longlong(b)));
+}
 constexpr int CRR_THREADS = 128;
 
 template <int C, int KIND>
@@ -60,12 +73,12 @@ __device__ __forceinline__ double crr_tree(int lane, int N, double S0, double K,
                 double ex;
                 if (KIND == KIND_BULL) {
                     X[c][q] *= d;
-                    ex = fmin(fmax(X[c][q] - K, 0.0), K2 - K);
+                    ex = min_nonneg(max_nonneg(X[c][q] - K, 0.0), K2 - K);
                 } else {
                     X[c][q] = fma(d, X[c][q], c0);
                     ex = X[c][q];
                 }
-                V[c][q] = fmax(ex, fma(pu, V[c][q], pd * vn));
+                V[c][q] = max_nonneg(ex, fma(pu, V[c][q], pd * vn));
             }
         }
     }

@@ -62,7 +62,20 @@ struct StripLaunchArgs {
     size_t ws_stride;    // bytes per warp
     int level;           // capacity level (0 = first pass; +1 = 4x arenas)
     int ctas;
+    // split mode (strips of one tree on different warps); split_S = 0: off
+    int split_S = 0;
+    int* progress = nullptr;
+    char* carry = nullptr;
+    size_t carry_stride = 0;
+    void* carena_split = nullptr;
+    int* carena_cnt = nullptr;
+    int carena_split_cap = 0;
 };
+size_t strip_carry_bytes(int N);
+int strip_split_arena_cap(int N);
+size_t strip_vtx_bytes();
+void tc_launch_split_expand(const int* items, const int* n_items, int S, int64_t max_items, int* out, int* n_out,
+                            cudaStream_t s);
 size_t strip_ws_bytes_per_warp(int N, int level);
 int strip_warps_per_cta();
 int strip_ctas_per_sm();

@@ -36,6 +36,8 @@
 // arenas (amtc_capi.cu), never truncating a function.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "amtc_internal.cuh"
 #include "amtc_option.cuh"
 #include "pwl_device.cuh"
@@ -134,6 +136,14 @@ struct StripLaunch {
     char* ws;
     StripCaps caps;
     StripLayout lay;
+    // split mode (one tree's strips on different warps): 0 = off, else strips per tree
+    int split_S;
+    int* progress;          // per (tree, strip): lowest level whose carry is published
+    char* carry;            // per (tree, strip): chdr | csl | cv, carry_stride bytes
+    size_t carry_stride, c_csl, c_cv;
+    Vtx* carena_split;      // per tree: carry arena, carena_split_cap vertices
+    int* carena_cnt;        // per tree: its bump counter
+    int carena_split_cap;
 };
 
 #define WS(T, field, q) reinterpret_cast<T*>(wb + L.lay.field + (size_t)(q) * L.lay.field##_ps)
@@ -267,8 +277,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
         it = __shfl_sync(FULL, it, 0);
         if (it >= *L.n_items) break;
         const int code = L.items[it];
-        const int64_t opt = code >> 1;
-        const bool seller = (code & 1) == 0;
+        const bool split = L.split_S > 0;
+        const int tree = split ? code / L.split_S : code;  // 2 option + party
+        const int s_first = split ? code % L.split_S : N / SW, s_last = split ? s_first : 0;
+        const int64_t opt = tree >> 1;
+        const bool seller = (tree & 1) == 0;
         OptionConsts oc;
         if (validate_option(L.in, opt, N, true, oc) != STATUS_OK) continue;  // status set by prepare
 
@@ -281,9 +294,49 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
         int maxn = 1;
         unsigned long long vsum = 0;
 
-        for (int s = N / SW; s >= 0 && !err; --s) {
+        for (int s = s_first; s >= s_last && !err; --s) {
             const int j0 = s * SW, j = j0 + lane;
             const int cout = s & 1, cin = cout ^ 1;
+            // carry columns: this strip's (out) and the strip to the right's (in)
+            int2* chdr_o;
+            double* csl_o;
+            Vtx* cv_o;
+            Vtx* ca_o;
+            int* ccnt;
+            int ccap;
+            const int2* chdr_i;
+            const double* csl_i;
+            const Vtx* cv_i;
+            const Vtx* ca_i;
+            volatile int* prog_in = nullptr;
+            volatile int* prog_out = nullptr;
+            if (split) {
+                char* co = L.carry + ((size_t)tree * L.split_S + s) * L.carry_stride;
+                char* ci = co + L.carry_stride;  // strip s+1 (read only when it exists)
+                chdr_o = reinterpret_cast<int2*>(co);
+                csl_o = reinterpret_cast<double*>(co + L.c_csl);
+                cv_o = reinterpret_cast<Vtx*>(co + L.c_cv);
+                chdr_i = reinterpret_cast<const int2*>(ci);
+                csl_i = reinterpret_cast<const double*>(ci + L.c_csl);
+                cv_i = reinterpret_cast<const Vtx*>(ci + L.c_cv);
+                ca_o = L.carena_split + (size_t)tree * L.carena_split_cap;
+                ca_i = ca_o;
+                ccnt = &L.carena_cnt[tree];
+                ccap = L.carena_split_cap;
+                prog_out = L.progress + (size_t)tree * L.split_S + s;
+                prog_in = prog_out + 1;
+            } else {
+                chdr_o = WS(int2, chdr, cout);
+                csl_o = WS(double, csl, cout);
+                cv_o = WS(Vtx, cv, cout);
+                ca_o = WS(Vtx, carena, cout);
+                chdr_i = WS(int2, chdr, cin);
+                csl_i = WS(double, csl, cin);
+                cv_i = WS(Vtx, cv, cin);
+                ca_i = WS(Vtx, carena, cin);
+                ccnt = &S.ccnt;
+                ccap = L.caps.carena_cap;
+            }
             // a2: leaves t = N+1, payoff (0,0): z = y^- S^a - y^+ S^b
             int my_n = 0, my_off = -1;
             double my_sl = 0.0;
@@ -333,10 +386,21 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
                 } else if (t == N) {
                     D = make_fn(&S.leaf31, 1, leaf31_sl, 1);  // the analytic leaf (N+1, j+1)
                 } else if (active) {
-                    const int2 h = WS(int2, chdr, cin)[t + 1];
-                    const double csl = WS(double, csl, cin)[t + 1];
-                    D = (h.y < 0) ? make_fn(WS(Vtx, cv, cin) + (size_t)(t + 1) * C, h.x, csl, 1)
-                                  : make_fn(WS(Vtx, carena, cin) + h.y, h.x, csl, 1);
+                    int pv = 0;
+                    if (prog_in) {  // split mode: wait until strip s+1 has published level t+1
+                        while ((pv = *prog_in) > t + 1) __nanosleep(32);
+                        __threadfence();
+                    }
+                    if (pv < 0) {  // strip s+1 failed (capacity): finish with a dummy, re-run later
+                        err |= DEV_OVERFLOW;
+                        D = make_fn(&S.leaf31, 1, leaf31_sl, 1);
+                    } else {
+                        const volatile int* hp = reinterpret_cast<const volatile int*>(&chdr_i[t + 1]);
+                        const int2 h = make_int2(hp[0], hp[1]);
+                        const double csl = *(volatile const double*)&csl_i[t + 1];
+                        D = (h.y < 0) ? make_fn(cv_i + (size_t)(t + 1) * C, h.x, csl, 1)
+                                      : make_fn(ca_i + h.y, h.x, csl, 1);
+                    }
                 } else {
                     D = make_fn(&S.leaf31, 0, 0.0, 1);
                 }
@@ -450,22 +514,27 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
                 {
                     const int c_n = __shfl_sync(FULL, my_n, 0);
                     const int c_off = __shfl_sync(FULL, my_off, 0);
-                    if (lane == 0) WS(double, csl, cout)[t] = my_sl;
+                    if (lane == 0) csl_o[t] = my_sl;
                     if (c_off < 0) {
-                        if (lane < c_n) WS(Vtx, cv, cout)[(size_t)t * C + lane] = S.row[lane * SW];
-                        if (lane == 0) WS(int2, chdr, cout)[t] = make_int2(c_n, -1);
+                        if (lane < c_n) cv_o[(size_t)t * C + lane] = S.row[lane * SW];
+                        if (lane == 0) chdr_o[t] = make_int2(c_n, -1);
                     } else {
                         int base = 0;
-                        if (lane == 0) base = atomicAdd(&S.ccnt, c_n);
+                        if (lane == 0) base = atomicAdd(ccnt, c_n);
                         base = __shfl_sync(FULL, base, 0);
-                        if (base + c_n > L.caps.carena_cap) {
+                        if (base + c_n > ccap) {
                             err |= DEV_OVERFLOW;
                         } else {
-                            Vtx* const ca = WS(Vtx, carena, cout) + base;
+                            Vtx* const ca = ca_o + base;
                             const Vtx* const ra = WS(Vtx, rarena, nxt) + c_off;
                             for (int i = lane; i < c_n; i += 32) ca[i] = ra[i];
-                            if (lane == 0) WS(int2, chdr, cout)[t] = make_int2(c_n, base);
+                            if (lane == 0) chdr_o[t] = make_int2(c_n, base);
                         }
+                    }
+                    if (prog_out) {  // split mode: publish level t to strip s-1
+                        __threadfence();
+                        __syncwarp();
+                        if (lane == 0) *prog_out = t;
                     }
                 }
                 if (lane == 0) S.rcnt[cur] = 0;  // level t+1's arena is dead
@@ -475,6 +544,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
                 __syncwarp();
             }
             __syncwarp();
+            if (prog_out && err && lane == 0) *prog_out = -1;  // never leave strip s-1 waiting
             if (s == 0 && !err) {
                 const Fn mine = (my_off < 0) ? make_fn(&S.row[lane], my_n, my_sl, SW)
                                              : make_fn(WS(Vtx, rarena, cur) + my_off, my_n, my_sl, 1);
@@ -552,6 +622,18 @@ StripCaps strip_caps(int N, int level) {
 
 size_t strip_ws_bytes_per_warp(int N, int level) { return strip_layout(N, strip_caps(N, level)).total; }
 
+// split mode: bytes of one strip's carry column (chdr | csl | cv) and the
+// per-tree carry arena (vertices)
+size_t strip_carry_bytes(int N) {
+    return align256(sizeof(int2) * (size_t)(N + 2)) + align256(sizeof(double) * (size_t)(N + 2)) +
+           align256(sizeof(Vtx) * (size_t)STRIP_C * (size_t)(N + 2));
+}
+int strip_split_arena_cap(int N) {
+    const int64_t v = 16 * (int64_t)(N + 2) * (N / SW + 1) + 65536;
+    return (int)std::min<int64_t>(v, (int64_t)1 << 30);
+}
+size_t strip_vtx_bytes() { return sizeof(Vtx); }
+
 int strip_warps_per_cta() { return STRIP_WARPS; }
 
 int strip_ctas_per_sm() {
@@ -573,6 +655,15 @@ int strip_launch(const StripLaunchArgs& a, cudaStream_t s) {
     L.ovf_count = a.ovf_count;
     L.vertex_sum = a.vertex_sum;
     L.ws = a.ws;
+    L.split_S = a.split_S;
+    L.progress = a.progress;
+    L.carry = a.carry;
+    L.carry_stride = a.carry_stride;
+    L.c_csl = align256(sizeof(int2) * (size_t)(a.N + 2));
+    L.c_cv = L.c_csl + align256(sizeof(double) * (size_t)(a.N + 2));
+    L.carena_split = reinterpret_cast<Vtx*>(a.carena_split);
+    L.carena_cnt = a.carena_cnt;
+    L.carena_split_cap = a.carena_split_cap;
     L.caps = strip_caps(a.N, a.level);
     L.lay = strip_layout(a.N, L.caps);
     if (L.lay.total != a.ws_stride) return STATUS_EINVAL;

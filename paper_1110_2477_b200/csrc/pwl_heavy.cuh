@@ -259,6 +259,19 @@ __device__ __forceinline__ double cross_at(const Line& A, const Line& B, double 
     return ref - (A.at(ref) - B.at(ref)) / (A.s - B.s);
 }
 
+// the crossing y of A with B (A.s < B.s: A comes from above; rising = true:
+// A.s > B.s, A comes from below) replaces nx if p_in < y < nx.  In exact
+// arithmetic y < nx iff A is already past B at a finite nx.
+__device__ __forceinline__ void try_cross(const Line& A, const Line& B, double ref, double p_in, double& nx,
+                                          bool rising) {
+    if (isfinite(nx)) {
+        const double a = A.at(nx), b = B.at(nx);
+        if (rising ? !(a > b) : !(a < b)) return;
+    }
+    const double y = cross_at(A, B, ref);
+    if (y > p_in && y < nx) nx = y;
+}
+
 // per-lane staging of output vertices (global scratch, lane-interleaved)
 struct Stage {
     Vtx* buf;  // STAGE x 32
@@ -308,19 +321,18 @@ __device__ __forceinline__ double emit_open(double a, double b, const Line& LW, 
         const Line Uq{c.ux, c.uf, us};
         double nx = b_in;
         // v switches to a line with a smaller slope that comes from above
-        if (vi != 1 && hasM && LM.s < V.s) { const double y = cross_at(LM, V, ref); if (y > p_in && y < nx) nx = y; }
-        if (vi != 2 && hasP && LP.s < V.s) { const double y = cross_at(LP, V, ref); if (y > p_in && y < nx) nx = y; }
-        if (vi != 0 && LW.s < V.s) { const double y = cross_at(LW, V, ref); if (y > p_in && y < nx) nx = y; }
+        // (each crossing is first screened by the sign of the difference at nx,
+        // so the division runs only for a crossing that can still win)
+        if (vi != 1 && hasM && LM.s < V.s) try_cross(LM, V, ref, p_in, nx, false);
+        if (vi != 2 && hasP && LP.s < V.s) try_cross(LP, V, ref, p_in, nx, false);
+        if (vi != 0 && LW.s < V.s) try_cross(LW, V, ref, p_in, nx, false);
         // u's kink
         if (pos < c.ux && c.ux < nx) nx = c.ux;
         // z's loser overtakes the winner
         {
             const Line& Wn = zU ? Uq : V;
             const Line& Ls = zU ? V : Uq;
-            if (c.seller ? (Ls.s > Wn.s) : (Ls.s < Wn.s)) {
-                const double y = cross_at(Ls, Wn, ref);
-                if (y > p_in && y < nx) nx = y;
-            }
+            if (c.seller ? (Ls.s > Wn.s) : (Ls.s < Wn.s)) try_cross(Ls, Wn, ref, p_in, nx, c.seller);
         }
         if (!(nx < b_in)) break;
         pos = nx;
@@ -1055,7 +1067,8 @@ __device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo,
         const double gl = has ? fma(-lo, wv.x, wv.f) : INFINITY;
         const double hl = has ? fma(-hi, wv.x, wv.f) : INFINITY;
         const double Mnext = fmin(excl_suffix_min(gl, lane), Mafter[blk]);  // g over later W vertices
-        const double Pl = fmin(excl_prefix_min(hl, lane), Pc);             // h over earlier W vertices
+        const double hpre = excl_prefix_min(hl, lane);
+        const double Pl = fmin(hpre, Pc);                                   // h over earlier W vertices
         const bool first_overall = has && j == 0;
         Stage st;
         st.buf = stage_buf;
@@ -1161,7 +1174,7 @@ __device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo,
             const double lxl = __shfl_sync(FULLM, lx, lastl < 0 ? 0 : lastl);
             if (lastl >= 0) last_x = lxl;
         }
-        Pc = fmin(Pc, warp_min(hl));
+        Pc = fmin(Pc, __shfl_sync(FULLM, fmin(hpre, hl), 31));
         __syncwarp();
     }
     if (err) return err;

@@ -212,3 +212,31 @@ def test_heavy_sawtooth_calls(api):
     # no representation bloat: vertex counts as in the oracle (kinks + 1), small slack
     for i, q in enumerate(want):
         assert got["max_bp"][i] <= 1.1 * (max(q.max_kinks_ask, q.max_kinks_bid) + 1) + 4, (i, got["max_bp"][i], q)
+
+
+@pytest.mark.parametrize("N", [64, 97, 300])
+def test_split_mode_matches_oracle(api, N):
+    """Strip-split mode (the strips of one tree on different warps, pipelined
+    through progress counters) against the oracle and against whole-tree mode."""
+    b = W.random_small(6, seed=5000 + N, k_max=0.05)
+    try:
+        api.debug_set_split_mode(1)
+        got, rc = api.price_american_tc_batch_host(b, N)
+        api.debug_set_split_mode(0)
+        ref, rc0 = api.price_american_tc_batch_host(b, N)
+    finally:
+        api.debug_set_split_mode(-1)
+    assert rc == 0 and rc0 == 0
+    assert_quotes(got, b, N)
+    np.testing.assert_allclose(got["ask"], ref["ask"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(got["bid"], ref["bid"], rtol=1e-12, atol=1e-12)
+
+
+def test_config5b_single_tree_split(api):
+    """BASELINE config 5b shape at a size the oracle finishes quickly (N=1200),
+    through the north-star single-option call (automatic split mode)."""
+    r = W.config5b().row(0)
+    N = 1200
+    q = api.price_american_tc(r["S0"], r["K"], r["T"], r["sigma"], r["R"], N, r["k"], api.PUT)
+    o = O.price_tc(_opt(r), N)
+    assert q["status"] == 0 and close(q["ask"], o.ask) and close(q["bid"], o.bid), (q, o)
