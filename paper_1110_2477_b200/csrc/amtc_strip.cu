@@ -120,7 +120,8 @@ struct StripSmem {
 
 struct CtaHdr {
     int active;  // warps of this CTA still working on items
-    int pad[3];
+    int posted;  // heavy nodes posted and not yet claimed (cheap poll for helpers)
+    int pad[2];
 };
 
 struct StripLaunch {
@@ -174,8 +175,8 @@ __device__ __forceinline__ Fn shfl_fn(const Fn& F, int src) {
 // (pwl_heavy.cuh) into the claimer's scratch and copied into the owner's row
 // arena.  Returns true if a node was served.
 template <int C, int B, int WARPS>
-__device__ __noinline__ bool serve_one(StripSmem<C, B>* all, int me, Vtx* hscr, int hcap, Vtx* zbuf, int zcap,
-                                       int lane) {
+__device__ __noinline__ bool serve_one(CtaHdr& H, StripSmem<C, B>* all, int me, Vtx* hscr, int hcap, Vtx* zbuf,
+                                       int zcap, int lane) {
     // candidate owner: the first warp (starting with this one) with posted nodes
     unsigned pw = 0;
     if (lane < WARPS) pw = *(volatile unsigned*)&all[(me + lane) % WARPS].post;
@@ -191,7 +192,11 @@ __device__ __noinline__ bool serve_one(StripSmem<C, B>* all, int me, Vtx* hscr, 
             while (cur) {
                 const unsigned bit = cur & (0u - cur);
                 const unsigned old = atomicAnd(&all[w].post, ~bit);
-                if (old & bit) { got = __ffs(bit) - 1; break; }
+                if (old & bit) {
+                    got = __ffs(bit) - 1;
+                    atomicSub(&H.posted, 1);
+                    break;
+                }
                 cur = old & ~bit;
             }
         }
@@ -264,7 +269,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
     double* const Dpow = WS1(double, dpow);
     Vtx* const hscr = WS1(Vtx, hscr);
     Vtx* const zbuf = WS1(Vtx, zbuf);
-    if (threadIdx.x == 0) H.active = WARPS;
+    if (threadIdx.x == 0) {
+        H.active = WARPS;
+        H.posted = 0;
+    }
     if (lane == 0) {
         S.post = 0u;
         S.done = 0;
@@ -367,12 +375,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
                 const int nxt = cur ^ 1;
                 const bool active = j <= t;
                 // help: serve one heavy node posted by another warp of the CTA
-                {
-                    unsigned pw = 0;
-                    if (lane < WARPS) pw = *(volatile unsigned*)&all[lane].post;
-                    if (__any_sync(FULL, pw != 0))
-                        serve_one<C, B, WARPS>(all, wib, hscr, L.caps.hscr_cap, zbuf, L.caps.zbuf_cap, lane);
-                }
+                if (*(volatile int*)&H.posted > 0)
+                    serve_one<C, B, WARPS>(H, all, wib, hscr, L.caps.hscr_cap, zbuf, L.caps.zbuf_cap, lane);
                 // children: up = own previous; down = lane+1's previous / carry / leaf
                 const int dn = __shfl_down_sync(FULL, my_n, 1);
                 const int doff = __shfl_down_sync(FULL, my_off, 1);
@@ -455,10 +459,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
                     }
                     __syncwarp();
                     __threadfence_block();
-                    if (lane == 0) atomicOr(&S.post, hmask);
+                    if (lane == 0) {
+                        atomicAdd(&H.posted, __popc(hmask));
+                        atomicOr(&S.post, hmask);
+                    }
                     __syncwarp();
                     while (*(volatile int*)&S.done > 0) {
-                        if (!serve_one<C, B, WARPS>(all, wib, hscr, L.caps.hscr_cap, zbuf, L.caps.zbuf_cap, lane))
+                        if (*(volatile int*)&H.posted <= 0 ||
+                            !serve_one<C, B, WARPS>(H, all, wib, hscr, L.caps.hscr_cap, zbuf, L.caps.zbuf_cap, lane))
                             __nanosleep(64);
                     }
                     __threadfence_block();
@@ -572,7 +580,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
     if (lane == 0) atomicSub(&H.active, 1);
     __syncwarp();
     while (*(volatile int*)&H.active > 0) {
-        if (!serve_one<C, B, WARPS>(all, wib, hscr, L.caps.hscr_cap, zbuf, L.caps.zbuf_cap, lane)) __nanosleep(256);
+        if (*(volatile int*)&H.posted <= 0 ||
+            !serve_one<C, B, WARPS>(H, all, wib, hscr, L.caps.hscr_cap, zbuf, L.caps.zbuf_cap, lane))
+            __nanosleep(1000);
     }
 }
 
