@@ -255,11 +255,24 @@ def run_amtc(args):
     total_opts = sum_over_ranks(float(n * args.steps), pg, dev)
     value = total_nodes / (total_ms / 1e3)
 
-    # roofline of the dominant kernel
+    # roofline of the dominant kernel: FP64 DFMA peak measured on this pool's
+    # B200s by tools/fp64_peak.cu (MEASURED_PEAKS.json has no FP64 entry);
+    # fallback: the unit-count derivation
     props = torch.cuda.get_device_properties(dev)
     sm_count = props.multi_processor_count
     clk = (clocks or {}).get("sm_max_mhz") or 1965.0
     peak_tflops = sm_count * FP64_LANES_PER_SM * 2 * clk * 1e6 / 1e12
+    peak_src = (f"derived: {sm_count} SMs x 64 FP64/clk x 2 x {clk:.0f} MHz "
+                "(no FP64 entry in MEASURED_PEAKS.json)")
+    fp64_file = os.path.join(ROOT, "profiles", "r01_fp64_peak.json")
+    if os.path.exists(fp64_file):
+        try:
+            m = json.load(open(fp64_file))
+            peak_tflops = float(m["fp64_tflops"])
+            peak_src = ("measured: DFMA throughput by tools/fp64_peak.cu on this pool's B200 "
+                        "(profiles/r01_fp64_peak.json; MEASURED_PEAKS.json has no FP64 entry)")
+        except Exception:
+            pass
     if args.config == 4:
         kern_ms = kernel_ms / args.steps
         flop = TC_FLOP_PER_CHILD_VERTEX * 2.0 * vertex_sum / args.steps
@@ -273,8 +286,7 @@ def run_amtc(args):
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
                 "frac": achieved / peak_tflops, "traffic": None, "kernel": kname,
                 "kernel_ms_per_step": kern_ms,
-                "peak_source": f"derived: {sm_count} SMs x 64 FP64/clk x 2 x {clk:.0f} MHz "
-                               "(no FP64 entry in MEASURED_PEAKS.json)",
+                "peak_source": peak_src,
                 "flop_model": ("12 flop per child vertex per node-update (DESIGN.md)" if args.config == 4
                                else "6 flop per CRR node-update (DESIGN.md)")}
     if args.config == 4:

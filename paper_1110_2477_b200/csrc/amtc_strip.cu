@@ -579,10 +579,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
     // no items left: serve the CTA's remaining heavy nodes until every warp is done
     if (lane == 0) atomicSub(&H.active, 1);
     __syncwarp();
+    unsigned nap = 256;  // exponential backoff while nothing is posted
     while (*(volatile int*)&H.active > 0) {
-        if (*(volatile int*)&H.posted <= 0 ||
-            !serve_one<C, B, WARPS>(H, all, wib, hscr, L.caps.hscr_cap, zbuf, L.caps.zbuf_cap, lane))
-            __nanosleep(1000);
+        if (*(volatile int*)&H.posted > 0 &&
+            serve_one<C, B, WARPS>(H, all, wib, hscr, L.caps.hscr_cap, zbuf, L.caps.zbuf_cap, lane)) {
+            nap = 256;
+        } else {
+            __nanosleep(nap);
+            nap = min(nap * 2, 32768u);
+        }
     }
 }
 

@@ -904,6 +904,10 @@ struct HWin {
     int ev[32];        // merged event k of the block: isU | idx << 1 | rank << 7
 };
 
+__device__ __forceinline__ Vtx shfl_vtx(const Vtx& v, int src) {
+    return Vtx{__shfl_sync(FULLM, v.x, src), __shfl_sync(FULLM, v.f, src), __shfl_sync(FULLM, v.s, src)};
+}
+
 __device__ __forceinline__ int rank_lt(const Vtx* w, double x) {  // #{m < 32 : w[1+m].x < x}
     int p = 0;
 #pragma unroll
@@ -976,14 +980,19 @@ __device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo,
     int a = 0, b = 0, nW = 0;
     double cx = -INFINITY;   // x of the last event of the previous block
     bool cwr = h.tailL_U;    // winner just right of it (first block: the left-tail winner)
+    const Vtx SENT{INFINITY, 0.0, 0.0};
     if (lane == 0) {
         Wn.u[0] = Vtx{U.v(0).x, U.v(0).f, U.sl};
         Wn.d[0] = Vtx{D.v(0).x, D.v(0).f, D.sl};
     }
+    Wn.u[1 + lane] = (lane < U.n) ? U.v(lane) : SENT;
+    Wn.d[1 + lane] = (lane < D.n) ? D.v(lane) : SENT;
+    // software pipeline: the 32 elements after each window are loaded one block
+    // ahead (registers), so no block waits on global memory
+    Vtx pu = (32 + lane < U.n) ? U.v(32 + lane) : SENT;
+    Vtx pd = (32 + lane < D.n) ? D.v(32 + lane) : SENT;
+    __syncwarp();
     for (int k0 = 0; k0 < nE; k0 += 32) {
-        Wn.u[1 + lane] = (a + lane < U.n) ? U.v(a + lane) : Vtx{INFINITY, 0.0, 0.0};
-        Wn.d[1 + lane] = (b + lane < D.n) ? D.v(b + lane) : Vtx{INFINITY, 0.0, 0.0};
-        __syncwarp();
         const int nrem = min(32, nE - k0);
         {
             const Vtx uu = Wn.u[1 + lane], dd = Wn.d[1 + lane];
@@ -1022,13 +1031,24 @@ __device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo,
         const int cU = __popc(bu), cD = __popc(bv) - cU;
         cx = __shfl_sync(FULLM, e.x, 31);
         cwr = __shfl_sync(FULLM, (int)wr, 31) != 0;
-        __syncwarp();
-        if (lane == 0) {
-            if (cU > 0) Wn.u[0] = Wn.u[cU];
-            if (cD > 0) Wn.d[0] = Wn.d[cD];
+        // shift the windows by the consumed elements, refill from the prefetch
+        {
+            const Vtx pu_s = shfl_vtx(pu, (lane + cU) & 31), pd_s = shfl_vtx(pd, (lane + cD) & 31);
+            const Vtx nu = (lane + cU < 32) ? Wn.u[1 + lane + cU] : pu_s;
+            const Vtx nd = (lane + cD < 32) ? Wn.d[1 + lane + cD] : pd_s;
+            const Vtx pvu = Wn.u[cU], pvd = Wn.d[cD];
+            __syncwarp();
+            Wn.u[1 + lane] = nu;
+            Wn.d[1 + lane] = nd;
+            if (lane == 0) {
+                Wn.u[0] = pvu;
+                Wn.d[0] = pvd;
+            }
         }
         a += cU;
         b += cD;
+        pu = (a + 32 + lane < U.n) ? U.v(a + 32 + lane) : SENT;
+        pd = (b + 32 + lane < D.n) ? D.v(b + 32 + lane) : SENT;
         __syncwarp();
     }
     if (nW == 0) return DEV_FALLBACK;  // W is a line: not a heavy node (caller falls back)
@@ -1038,12 +1058,15 @@ __device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo,
     // ---- sweep B: Mafter[b] = min of g over blocks > b ----
     {
         double Mc = INFINITY;
+        int j = (nb - 1) * 32 + lane;
+        Vtx v = (j < nW) ? Wb[j] : SENT;
         for (int blk = nb - 1; blk >= 0; --blk) {
-            const int j = blk * 32 + lane;
-            double g = INFINITY;
-            if (j < nW) { const Vtx v = Wb[j]; g = fma(-lo, v.x, v.f); }
+            const Vtx vn = (blk > 0) ? Wb[j - 32] : SENT;  // prefetch the block to the left
+            const double g = (j < nW) ? fma(-lo, v.x, v.f) : INFINITY;
             if (lane == 0) Mafter[blk] = Mc;
             Mc = fmin(Mc, warp_min(g));
+            v = vn;
+            j -= 32;
         }
     }
     __syncwarp();
@@ -1056,14 +1079,19 @@ __device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo,
     double Pc = INFINITY;
     double s_in = lo;           // z's slope arriving from the left (z's left tail is lo)
     double last_x = -INFINITY;  // the last vertex written (earlier blocks)
+    Vtx wv_nx = (lane < nW) ? Wb[lane] : SENT;
+    double prev_s = slW;  // slope right of the last W vertex of the previous block
     for (int blk = 0; blk < nb; ++blk) {
         const int j = blk * 32 + lane;
         const bool has = j < nW;
-        Vtx wv = has ? Wb[j] : Vtx{INFINITY, 0.0, 0.0};
+        const Vtx wv = wv_nx;
+        wv_nx = (j + 32 < nW) ? Wb[j + 32] : SENT;  // prefetch the next block
         double sL = __shfl_up_sync(FULLM, wv.s, 1);
-        if (lane == 0) sL = blk == 0 ? slW : Wb[j - 1].s;
+        if (lane == 0) sL = prev_s;
+        prev_s = __shfl_sync(FULLM, wv.s, 31);
         double xn = __shfl_down_sync(FULLM, wv.x, 1);
-        if (lane == 31) xn = (j + 1 < nW) ? Wb[j + 1].x : INFINITY;
+        const double xn31 = __shfl_sync(FULLM, wv_nx.x, 0);
+        if (lane == 31) xn = xn31;
         const double gl = has ? fma(-lo, wv.x, wv.f) : INFINITY;
         const double hl = has ? fma(-hi, wv.x, wv.f) : INFINITY;
         const double Mnext = fmin(excl_suffix_min(gl, lane), Mafter[blk]);  // g over later W vertices
