@@ -340,12 +340,111 @@ def run_amtc(args):
     return 0
 
 
+def run_tree(args):
+    """Configs 1, 3, 5 (single trees).  Config 5a (CRR, N = 100000) runs sharded
+    over all ranks through amtc_price_tree_sharded (NCCL halo exchange, strong
+    scaling); configs 1, 3 and 5b run the north-star single-option call (strip-
+    split mode) on rank 0.  Timer: host wall clock around the synchronous C-ABI
+    calls (they include the host-side band loop), max over ranks."""
+    import torch
+    import oracle as O_  # cpu_baseline leg only
+    from paper_1110_2477_b200 import api, build, workloads as W
+    world, rank, local, pg = setup_dist()
+    assert torch.cuda.is_available(), "bench.py needs a CUDA device"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    build.build()
+    api.lib()
+    comm = None
+    if args.config == 5:
+        r = W.config5a().row(0)
+        N = W.CONFIG5A_N
+        if world > 1:
+            comm, _, _ = api.comm_from_torch_dist()
+        def step():
+            q = api.price_tree_sharded(r["S0"], r["K"], r["T"], r["sigma"], r["R"], N, 0.0, api.PUT,
+                                       comm=comm, rank=rank, nranks=world)
+            assert q["status"] == 0, q
+        nodes = crr_nodes(N)
+        desc = f"config5a: one American put tree, k=0 CRR, N={N}, sharded over {world} GPU(s) (NCCL halo per band)"
+        scaling = "strong"
+        cpu_sample = (O_.Option(r["S0"], r["K"], r["T"], r["sigma"], r["R"], 0.0, O_.PUT), 20000, "crr")
+    else:
+        if args.config == 1:
+            trees = [(W.config1().row(0), W.CONFIG1_N)]
+            desc = "config1: Example 5.1 put, N=100, ask+bid (north-star single call)"
+        else:
+            trees = [(b.row(0), N_) for b, N_ in W.config3()]
+            desc = "config3: put+call x k in {0,.0025,.005,.01,.02} x N in {250..2000}, 50 single trees"
+        def step():
+            if rank != 0:
+                return
+            for row, N_ in trees:
+                q = api.price_american_tc(row["S0"], row["K"], row["T"], row["sigma"], row["R"], N_, row["k"],
+                                          row["kind"], row["K2"])
+                assert q["status"] == 0, q
+        nodes = sum(tc_nodes(N_) for _, N_ in trees)
+        scaling = "weak"
+        row0, N0 = trees[0]
+        cpu_sample = (O_.Option(row0["S0"], row0["K"], row0["T"], row0["sigma"], row0["R"], row0["k"], row0["kind"],
+                                row0["K2"]), N0, "tc")
+        N = max(N_ for _, N_ in trees)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if pg is not None:
+        pg.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    times = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        step()
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    clocks = sampler.stop() if sampler else None
+    tot = max_over_ranks(float(np.sum(times)), pg, dev)
+    value = nodes * args.steps / tot
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        opt, Ns, kind = cpu_sample
+        t0 = time.perf_counter()
+        if kind == "crr":
+            O_.price_crr(opt, Ns)
+            cn = crr_nodes(Ns)
+        else:
+            O_.price_tc(opt, Ns)
+            cn = tc_nodes(Ns)
+        dt = time.perf_counter() - t0
+        cpu = {"value": cn / dt, "unit": "node-updates/s", "cores": 1, "kind": "oracle",
+               "sample": f"one tree of the workload at N={Ns}, single thread, {dt:.2f} s"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "node-updates/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+                "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": desc, "N": N, "node_updates_per_step": nodes,
+                           "timer": "host wall clock around synchronous C-ABI calls, max over ranks",
+                           "l2": "inputs are scalars; levels live in HBM/L2 between bands"},
+                "roofline": None, "cpu_baseline": cpu, "e2e": None, "clocks": clocks,
+                "step_ms": [1e3 * t for t in times]}
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        api.comm_destroy(comm)
+    if pg is not None:
+        pg.barrier()
+        pg.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=4, choices=[2, 4])
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="amtc", choices=["amtc", "reference"])
     ap.add_argument("--ref-options", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -353,6 +452,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.config in (1, 3, 5):
+        return run_tree(args)
     return run_amtc(args)
 
 

@@ -19,7 +19,10 @@ for tl in [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "64,32,16,8,12
     torch.cuda.synchronize(); dt = time.time() - t
     q = api.quotes_to_numpy(out)
     if ref is None: ref = q
-    d = float(np.max(np.abs(q["bid"] - ref["bid"]) / (np.abs(ref["bid"]) + 1e-10)))
+    dd = np.abs(q["bid"] - ref["bid"]) - (1e-9 * np.abs(ref["bid"]) + 1e-10)
+    i = int(np.argmax(dd))
+    d = {"worst_excess_over_tol": float(dd[i]), "i": i, "bid": float(q["bid"][i]), "ref": float(ref["bid"][i]),
+         "max_abs_ask": float(np.max(np.abs(q["ask"] - ref["ask"])))}
     print(json.dumps({"tl": tl, "n": n, "s": round(dt, 4), "rc": rc, "stats": api.tc_last_stats(),
                       "max_bp": int(q["max_bp"].max()), "max_rel_vs_first": d}), flush=True)
 api.debug_set_heavy_threshold(0)
