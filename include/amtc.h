@@ -188,6 +188,12 @@ void amtc_debug_set_heavy_threshold(int tl);
    the resident warps), 0 never, 1 whenever it fits in memory. */
 void amtc_debug_set_split_mode(int mode);
 
+/* TESTING HOOK: 1 (default) runs the items that never grow heavy node
+   functions (sellers, put buyers) on the light kernel variant (no tier 3,
+   higher occupancy) before the full kernel; 0 runs everything on the full
+   kernel. */
+void amtc_debug_set_light_kernel(int on);
+
 #ifdef __cplusplus
 }
 #endif

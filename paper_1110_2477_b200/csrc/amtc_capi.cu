@@ -56,8 +56,15 @@ struct DevState {
     std::mutex mu;
     DevBuf items[2], cls, small, ws, stage_in, stage_out;
     DevBuf sp_items, sp_progress, sp_carry, sp_arena, sp_cnt;  // split mode
+    size_t budget = 0;  // cached workspace budget (bytes)
+    void* h_stage = nullptr;  // pinned host staging of small host batches
+    size_t h_stage_bytes = 0;
+    size_t held() const {
+        return ws.bytes + sp_items.bytes + sp_progress.bytes + sp_carry.bytes + sp_arena.bytes + sp_cnt.bytes;
+    }
     int sm_count = 0;
     int occupancy = 0;
+    int light_occupancy = 0;
     // stats of the last TC batch
     unsigned long long vertex_sum = 0;
     int passes = 0;
@@ -91,6 +98,8 @@ enum { SM_HIST = 0, SM_WORK = TC_CLASSES + 1, SM_OVF0, SM_OVF1, SM_WORST, SM_SPL
 
 // split mode policy (testing hook amtc_debug_set_split_mode): -1 auto, 0 off, 1 on when it fits
 static int g_split_mode = -1;
+// light kernel for class-0 items (testing hook amtc_debug_set_light_kernel)
+static int g_light_kernel = 1;
 
 // solver passes: every item first runs at capacity level 0; items that
 // overflowed a capacity (arena, scratch) are re-run at the next level (4x the
@@ -109,6 +118,7 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
     if (!st->sm_count) {
         AMTC_CUDA(cudaDeviceGetAttribute(&st->sm_count, cudaDevAttrMultiProcessorCount, dev));
         st->occupancy = strip_ctas_per_sm();
+        st->light_occupancy = strip_light_ctas_per_sm();
         if (st->occupancy < 1) {
             g_last_error = "strip solver cannot be resident on this device";
             return STATUS_ECUDA;
@@ -128,9 +138,15 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
     AMTC_CUDA(cudaGetLastError());
     AMTC_CUDA(cudaMemsetAsync(small + SM_VSUM, 0, sizeof(unsigned long long), s));
 
-    size_t free_b = 0, total_b = 0;
-    AMTC_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const size_t budget = std::min<size_t>((size_t)(0.6 * (double)(free_b + st->ws.bytes)), (size_t)48 << 30);
+    // workspace budget: 60% of (free + what this library already holds), at most
+    // 48 GB; cudaMemGetInfo is queried once per device and refreshed only when
+    // a call would need more than the cached budget allows
+    if (!st->budget) {
+        size_t free_b = 0, total_b = 0;
+        AMTC_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        st->budget = std::min<size_t>((size_t)(0.6 * (double)(free_b + st->held())), (size_t)48 << 30);
+    }
+    const size_t budget = st->budget;
 
     const int* q_items = static_cast<int*>(st->items[0].p);
     const int* q_count = small + SM_HIST + TC_CLASSES;  // total valid items
@@ -227,12 +243,42 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
         AMTC_CUDA(cudaMemsetAsync(small + SM_WORK, 0, sizeof(int), s));
         AMTC_CUDA(cudaMemsetAsync(ovf_count, 0, sizeof(int), s));
         AMTC_CUDA(cudaEventRecord(st->ev[2 * passes], s));
+        const bool light_pass = level == 0 && g_light_kernel && st->light_occupancy > 0;
+        if (light_pass) {
+            // class-0 items (sellers, put buyers) first, on the light kernel:
+            // items [hist[1], total) of the heavy-first queue
+            const size_t wsl = strip_ws_bytes_per_warp_light(N);
+            const int lw = strip_light_warps_per_cta();
+            int64_t lctas = (int64_t)st->sm_count * st->light_occupancy;
+            lctas = std::min<int64_t>(lctas, (queued + lw - 1) / lw);
+            lctas = std::min<int64_t>(lctas, (int64_t)(st->ws.bytes / (wsl * lw)));
+            if (lctas >= 1) {
+                StripLaunchArgs A;
+                A.in = in;
+                A.N = N;
+                A.out = out;
+                A.items = q_items;
+                A.item_lo = small + SM_HIST + 1;
+                A.n_items = q_count;
+                A.work_counter = small + SM_WORK;
+                A.ovf_items = ovf_items;
+                A.ovf_count = ovf_count;
+                A.vertex_sum = reinterpret_cast<unsigned long long*>(small + SM_VSUM);
+                A.ws = static_cast<char*>(st->ws.p);
+                A.ws_stride = wsl;
+                A.level = 0;
+                A.ctas = (int)lctas;
+                A.light = true;
+                if (strip_launch(A, s) != STATUS_OK) return cuda_fail(cudaGetLastError(), "light strip_kernel launch");
+                AMTC_CUDA(cudaMemsetAsync(small + SM_WORK, 0, sizeof(int), s));
+            }
+        }
         StripLaunchArgs A;
         A.in = in;
         A.N = N;
         A.out = out;
         A.items = q_items;
-        A.n_items = q_count;
+        A.n_items = light_pass ? small + SM_HIST + 1 : q_count;  // the light pass took class 0
         A.work_counter = small + SM_WORK;
         A.ovf_items = ovf_items;
         A.ovf_count = ovf_count;
@@ -283,6 +329,28 @@ static int stage_in(DevState* st, const amtc_batch_soa* h, int64_t n, amtc_batch
     double* f = reinterpret_cast<double*>(base);
     const double* src[7] = {h->S0, h->K, h->K2, h->T, h->sigma, h->R, h->k};
     const double** dst[7] = {&d->S0, &d->K, &d->K2, &d->T, &d->sigma, &d->R, &d->k};
+    if (soa_bytes(n) <= ((size_t)1 << 20)) {
+        // small batch (e.g. the north-star single option): pack into pinned
+        // memory and copy once
+        const size_t need = soa_bytes(n);
+        if (st->h_stage_bytes < need) {
+            if (st->h_stage) cudaFreeHost(st->h_stage);
+            st->h_stage = nullptr;
+            st->h_stage_bytes = 0;
+            AMTC_CUDA(cudaMallocHost(&st->h_stage, (size_t)1 << 20));
+            st->h_stage_bytes = (size_t)1 << 20;
+        }
+        double* hf = static_cast<double*>(st->h_stage);
+        for (int a = 0; a < 7; ++a) {
+            if (src[a]) std::memcpy(hf + a * n, src[a], sizeof(double) * n);
+            *dst[a] = src[a] ? f + a * n : nullptr;
+        }
+        std::memcpy(reinterpret_cast<int32_t*>(hf + 7 * n), h->kind, sizeof(int32_t) * n);
+        AMTC_CUDA(cudaMemcpyAsync(f, hf, need, cudaMemcpyHostToDevice, s));
+        AMTC_CUDA(cudaStreamSynchronize(s));  // the pinned buffer is reused by the next call
+        d->kind = reinterpret_cast<int32_t*>(f + 7 * n);
+        return STATUS_OK;
+    }
     for (int a = 0; a < 7; ++a) {
         if (src[a]) {
             AMTC_CUDA(cudaMemcpyAsync(f + a * n, src[a], sizeof(double) * n, cudaMemcpyHostToDevice, s));
@@ -420,6 +488,8 @@ const char* amtc_last_error(void) { return g_last_error.c_str(); }
 void amtc_debug_set_heavy_threshold(int tl) { strip_set_heavy_threshold(tl); }
 
 void amtc_debug_set_split_mode(int mode) { g_split_mode = mode < 0 ? -1 : (mode ? 1 : 0); }
+
+void amtc_debug_set_light_kernel(int on) { g_light_kernel = on ? 1 : 0; }
 
 int64_t amtc_launch_count(void) { return g_launches.load(); }
 

@@ -70,7 +70,13 @@ struct StripLaunchArgs {
     void* carena_split = nullptr;
     int* carena_cnt = nullptr;
     int carena_split_cap = 0;
+    // light kernel (no tier 3) and the first item of the launch (device pointer)
+    bool light = false;
+    const int* item_lo = nullptr;
 };
+size_t strip_ws_bytes_per_warp_light(int N);
+int strip_light_warps_per_cta();
+int strip_light_ctas_per_sm();
 size_t strip_carry_bytes(int N);
 int strip_split_arena_cap(int N);
 size_t strip_vtx_bytes();

@@ -102,10 +102,17 @@ struct HMail {
 
 // per-warp shared memory
 template <int C, int B>
-struct StripSmem {
+struct StripSmemBase {
     Vtx row[C * SW];  // lane-interleaved slots: vertex i of lane l at row[i * 32 + l]
     Vtx s0[B * SW];   // lane-interleaved scratch of the node update (A of pass 1)
     Vtx leaf31;       // lane 31's down child at t = N (an analytic leaf)
+    int rcnt[2];      // row arena bump counters
+    int ccnt;         // carry arena bump counter (current strip)
+    int zcnt;         // scratch counter of the fallback heavy update
+};
+// HEAVY = true: the tier-3 parts (the light-only kernel variant omits them)
+template <int C, int B, bool HEAVY = true>
+struct StripSmem : StripSmemBase<C, B> {
     heavy::HWin hw;   // merge windows of the tier-3 (heavy) node update
     HMail mail[SW];   // this warp's posted heavy nodes (one per lane)
     Vtx* h_arena;     // where their results go (this warp's next row arena) ...
@@ -113,10 +120,9 @@ struct StripSmem {
     int h_acap, h_seller;
     unsigned post;    // posted, not yet claimed heavy lanes
     int done;         // posted, not yet completed
-    int rcnt[2];      // row arena bump counters
-    int ccnt;         // carry arena bump counter (current strip)
-    int zcnt;         // scratch counter of the fallback heavy update
 };
+template <int C, int B>
+struct StripSmem<C, B, false> : StripSmemBase<C, B> {};
 
 struct CtaHdr {
     int active;  // warps of this CTA still working on items
@@ -145,6 +151,7 @@ struct StripLaunch {
     Vtx* carena_split;      // per tree: carry arena, carena_split_cap vertices
     int* carena_cnt;        // per tree: its bump counter
     int carena_split_cap;
+    const int* item_lo;     // device: first item index of this launch (nullptr: 0)
 };
 
 #define WS(T, field, q) reinterpret_cast<T*>(wb + L.lay.field + (size_t)(q) * L.lay.field##_ps)
@@ -175,7 +182,7 @@ __device__ __forceinline__ Fn shfl_fn(const Fn& F, int src) {
 // (pwl_heavy.cuh) into the claimer's scratch and copied into the owner's row
 // arena.  Returns true if a node was served.
 template <int C, int B, int WARPS>
-__device__ __noinline__ bool serve_one(CtaHdr& H, StripSmem<C, B>* all, int me, Vtx* hscr, int hcap, Vtx* zbuf,
+__device__ __noinline__ bool serve_one(CtaHdr& H, StripSmem<C, B, true>* all, int me, Vtx* hscr, int hcap, Vtx* zbuf,
                                        int zcap, int lane) {
     // candidate owner: the first warp (starting with this one) with posted nodes
     unsigned pw = 0;
@@ -204,7 +211,7 @@ __device__ __noinline__ bool serve_one(CtaHdr& H, StripSmem<C, B>* all, int me, 
         if (got >= 0) { owner = w; ol = got; }
     }
     if (owner < 0) return false;
-    StripSmem<C, B>& O = all[owner];
+    StripSmem<C, B, true>& O = all[owner];
     const HMail& M = O.mail[ol];
     const Fn U = make_fn(M.up, M.un, M.usl, M.ustr), D = make_fn(M.dp, M.dn, M.dsl, M.dstr);
     const bool seller = O.h_seller != 0;
@@ -256,13 +263,13 @@ __device__ __noinline__ int root_phase(Fn mine, OptionConsts oc, bool seller, Qu
     return DEV_OK;
 }
 
-template <int C, int B, int WARPS, int MINB>
+template <int C, int B, int WARPS, int MINB, bool HEAVY>
 __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_constant__ StripLaunch L) {
     extern __shared__ __align__(16) char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     CtaHdr& H = *reinterpret_cast<CtaHdr*>(smem_raw);
-    StripSmem<C, B>* const all = reinterpret_cast<StripSmem<C, B>*>(smem_raw + sizeof(CtaHdr));
-    StripSmem<C, B>& S = all[wib];
+    StripSmem<C, B, HEAVY>* const all = reinterpret_cast<StripSmem<C, B, HEAVY>*>(smem_raw + sizeof(CtaHdr));
+    StripSmem<C, B, HEAVY>& S = all[wib];
     const int N = L.N;
     char* const wb = L.ws + (size_t)(blockIdx.x * WARPS + wib) * L.lay.total;
     double* const Epow = WS1(double, epow);
@@ -273,15 +280,18 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
         H.active = WARPS;
         H.posted = 0;
     }
-    if (lane == 0) {
-        S.post = 0u;
-        S.done = 0;
+    if constexpr (HEAVY) {
+        if (lane == 0) {
+            S.post = 0u;
+            S.done = 0;
+        }
     }
     __syncthreads();
 
+    const int item_lo = L.item_lo ? *L.item_lo : 0;
     for (;;) {
         int it = 0;
-        if (lane == 0) it = atomicAdd(L.work_counter, 1);
+        if (lane == 0) it = item_lo + atomicAdd(L.work_counter, 1);
         it = __shfl_sync(FULL, it, 0);
         if (it >= *L.n_items) break;
         const int code = L.items[it];
@@ -375,8 +385,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
                 const int nxt = cur ^ 1;
                 const bool active = j <= t;
                 // help: serve one heavy node posted by another warp of the CTA
-                if (*(volatile int*)&H.posted > 0)
-                    serve_one<C, B, WARPS>(H, all, wib, hscr, L.caps.hscr_cap, zbuf, L.caps.zbuf_cap, lane);
+                if constexpr (HEAVY) {
+                    if (*(volatile int*)&H.posted > 0)
+                        serve_one<C, B, WARPS>(H, all, wib, hscr, L.caps.hscr_cap, zbuf, L.caps.zbuf_cap, lane);
+                }
                 // children: up = own previous; down = lane+1's previous / carry / leaf
                 const int dn = __shfl_down_sync(FULL, my_n, 1);
                 const int doff = __shfl_down_sync(FULL, my_off, 1);
@@ -441,9 +453,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
                     if (heavy) where = 0;
                 }
                 // tier 3: post this level's heavy nodes to the CTA and serve until they are done
-                const unsigned hmask = __ballot_sync(FULL, heavy);
                 int h_n = 0, h_off = 0;
-                if (hmask) {
+                if constexpr (!HEAVY) {
+                    if (heavy) err |= DEV_OVERFLOW;  // light-only kernel: re-run by the full kernel
+                } else if (const unsigned hmask = __ballot_sync(FULL, heavy)) {
                     if (heavy) {
                         HMail& m = S.mail[lane];
                         m.up = U.p; m.un = U.n; m.usl = U.sl; m.ustr = (short)U.stride;
@@ -577,16 +590,18 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
         __syncwarp();
     }
     // no items left: serve the CTA's remaining heavy nodes until every warp is done
-    if (lane == 0) atomicSub(&H.active, 1);
-    __syncwarp();
-    unsigned nap = 256;  // exponential backoff while nothing is posted
-    while (*(volatile int*)&H.active > 0) {
-        if (*(volatile int*)&H.posted > 0 &&
-            serve_one<C, B, WARPS>(H, all, wib, hscr, L.caps.hscr_cap, zbuf, L.caps.zbuf_cap, lane)) {
-            nap = 256;
-        } else {
-            __nanosleep(nap);
-            nap = min(nap * 2, 32768u);
+    if constexpr (HEAVY) {
+        if (lane == 0) atomicSub(&H.active, 1);
+        __syncwarp();
+        unsigned nap = 256;  // exponential backoff while nothing is posted
+        while (*(volatile int*)&H.active > 0) {
+            if (*(volatile int*)&H.posted > 0 &&
+                serve_one<C, B, WARPS>(H, all, wib, hscr, L.caps.hscr_cap, zbuf, L.caps.zbuf_cap, lane)) {
+                nap = 256;
+            } else {
+                __nanosleep(nap);
+                nap = min(nap * 2, 32768u);
+            }
         }
     }
 }
@@ -594,15 +609,25 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-// one CTA of 16 warps per SM: the CTA is the work-sharing domain of tier 3
+// full kernel: one CTA of 16 warps per SM (the CTA is the work-sharing domain of
+// tier 3).  Light kernel: no tier 3, three CTAs of 8 warps per SM (24 warps,
+// <= 85 registers), for the items that never grow heavy nodes (every seller,
+// every put buyer: DESIGN.md section 5); a heavy node there aborts the item,
+// which the full kernel re-runs.
 constexpr int STRIP_C = 6, STRIP_B = 6, STRIP_WARPS = 16, STRIP_MINB = 1;
-#define STRIP_KERNEL strip_kernel<STRIP_C, STRIP_B, STRIP_WARPS, STRIP_MINB>
-constexpr size_t STRIP_SMEM = sizeof(CtaHdr) + sizeof(StripSmem<STRIP_C, STRIP_B>) * STRIP_WARPS;
+constexpr int LIGHT_WARPS = 8, LIGHT_MINB = 3;
+#define STRIP_KERNEL strip_kernel<STRIP_C, STRIP_B, STRIP_WARPS, STRIP_MINB, true>
+#define LIGHT_KERNEL strip_kernel<STRIP_C, STRIP_B, LIGHT_WARPS, LIGHT_MINB, false>
+constexpr size_t STRIP_SMEM = sizeof(CtaHdr) + sizeof(StripSmem<STRIP_C, STRIP_B, true>) * STRIP_WARPS;
+constexpr size_t LIGHT_SMEM = sizeof(CtaHdr) + sizeof(StripSmem<STRIP_C, STRIP_B, false>) * LIGHT_WARPS;
 
 static int strip_set_smem() {
     static int done = 0;
     if (!done) {
         if (cudaFuncSetAttribute(STRIP_KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)STRIP_SMEM) !=
+            cudaSuccess)
+            return STATUS_ECUDA;
+        if (cudaFuncSetAttribute(LIGHT_KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LIGHT_SMEM) !=
             cudaSuccess)
             return STATUS_ECUDA;
         done = 1;
@@ -635,7 +660,25 @@ StripCaps strip_caps(int N, int level) {
     return c;
 }
 
+// the light kernel: no tier 3, small arenas (its functions stay below ~10 vertices)
+static StripCaps strip_caps_light(int N) {
+    StripCaps c = strip_caps(N, 0);
+    c.rarena_cap = 8 * (N + 2) + 4096;
+    c.carena_cap = 8 * (N + 2) + 4096;
+    c.hscr_cap = 0;
+    c.zbuf_cap = 0;
+    return c;
+}
+
 size_t strip_ws_bytes_per_warp(int N, int level) { return strip_layout(N, strip_caps(N, level)).total; }
+size_t strip_ws_bytes_per_warp_light(int N) { return strip_layout(N, strip_caps_light(N)).total; }
+int strip_light_warps_per_cta() { return LIGHT_WARPS; }
+int strip_light_ctas_per_sm() {
+    int b = 0;
+    if (strip_set_smem() != STATUS_OK) return 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, LIGHT_KERNEL, LIGHT_WARPS * 32, LIGHT_SMEM);
+    return b;
+}
 
 // split mode: bytes of one strip's carry column (chdr | csl | cv) and the
 // per-tree carry arena (vertices)
@@ -679,11 +722,13 @@ int strip_launch(const StripLaunchArgs& a, cudaStream_t s) {
     L.carena_split = reinterpret_cast<Vtx*>(a.carena_split);
     L.carena_cnt = a.carena_cnt;
     L.carena_split_cap = a.carena_split_cap;
-    L.caps = strip_caps(a.N, a.level);
+    L.item_lo = a.item_lo;
+    L.caps = a.light ? strip_caps_light(a.N) : strip_caps(a.N, a.level);
     L.lay = strip_layout(a.N, L.caps);
     if (L.lay.total != a.ws_stride) return STATUS_EINVAL;
     if (strip_set_smem() != STATUS_OK) return STATUS_ECUDA;
-    STRIP_KERNEL<<<a.ctas, STRIP_WARPS * 32, STRIP_SMEM, s>>>(L);
+    if (a.light) LIGHT_KERNEL<<<a.ctas, LIGHT_WARPS * 32, LIGHT_SMEM, s>>>(L);
+    else STRIP_KERNEL<<<a.ctas, STRIP_WARPS * 32, STRIP_SMEM, s>>>(L);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? STATUS_OK : STATUS_ECUDA;
 }

@@ -240,3 +240,23 @@ def test_config5b_single_tree_split(api):
     q = api.price_american_tc(r["S0"], r["K"], r["T"], r["sigma"], r["R"], N, r["k"], api.PUT)
     o = O.price_tc(_opt(r), N)
     assert q["status"] == 0 and close(q["ask"], o.ask) and close(q["bid"], o.bid), (q, o)
+
+
+def test_light_kernel_matches_full_kernel(api):
+    """Sellers and put buyers run on the light kernel variant by default; the
+    full kernel must give the same prices (and both match the oracle)."""
+    b = W.random_small(64, seed=6100, k_max=0.05)
+    N = 150
+    try:
+        api.debug_set_split_mode(0)
+        api.debug_set_light_kernel(False)
+        ref, rc0 = api.price_american_tc_batch_host(b, N)
+        api.debug_set_light_kernel(True)
+        got, rc = api.price_american_tc_batch_host(b, N)
+    finally:
+        api.debug_set_light_kernel(True)
+        api.debug_set_split_mode(-1)
+    assert rc == 0 and rc0 == 0
+    np.testing.assert_allclose(got["ask"], ref["ask"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(got["bid"], ref["bid"], rtol=1e-12, atol=1e-12)
+    assert_quotes(got, b, N)
