@@ -56,11 +56,15 @@ struct DevState {
     std::mutex mu;
     DevBuf items[2], cls, small, ws, stage_in, stage_out;
     DevBuf sp_items, sp_progress, sp_carry, sp_arena, sp_cnt;  // split mode
+    DevBuf ws_light;                                          // light-kernel workspaces
+    cudaStream_t s2 = nullptr;                                // light-kernel stream
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     size_t budget = 0;  // cached workspace budget (bytes)
     void* h_stage = nullptr;  // pinned host staging of small host batches
     size_t h_stage_bytes = 0;
     size_t held() const {
-        return ws.bytes + sp_items.bytes + sp_progress.bytes + sp_carry.bytes + sp_arena.bytes + sp_cnt.bytes;
+        return ws.bytes + sp_items.bytes + sp_progress.bytes + sp_carry.bytes + sp_arena.bytes + sp_cnt.bytes +
+               ws_light.bytes;
     }
     int sm_count = 0;
     int occupancy = 0;
@@ -94,7 +98,8 @@ static bool soa_ok(const amtc_batch_soa* b) {
 }
 
 // small device scratch layout (ints)
-enum { SM_HIST = 0, SM_WORK = TC_CLASSES + 1, SM_OVF0, SM_OVF1, SM_WORST, SM_SPLITN, SM_VSUM = 32, SM_INTS = 64 };
+enum { SM_HIST = 0, SM_WORK = TC_CLASSES + 1, SM_OVF0, SM_OVF1, SM_WORST, SM_SPLITN, SM_WORK2, SM_VSUM = 32,
+       SM_INTS = 64 };
 
 // split mode policy (testing hook amtc_debug_set_split_mode): -1 auto, 0 off, 1 on when it fits
 static int g_split_mode = -1;
@@ -243,34 +248,43 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
         AMTC_CUDA(cudaMemsetAsync(small + SM_WORK, 0, sizeof(int), s));
         AMTC_CUDA(cudaMemsetAsync(ovf_count, 0, sizeof(int), s));
         AMTC_CUDA(cudaEventRecord(st->ev[2 * passes], s));
-        const bool light_pass = level == 0 && g_light_kernel && st->light_occupancy > 0;
+        bool light_pass = level == 0 && g_light_kernel && st->light_occupancy > 0;
+        StripLaunchArgs AL;
         if (light_pass) {
-            // class-0 items (sellers, put buyers) first, on the light kernel:
-            // items [hist[1], total) of the heavy-first queue
+            // class-0 items (sellers, put buyers: items [hist[1], total) of the
+            // heavy-first queue) run on the light kernel, on a second stream, so
+            // its CTAs take over the SMs the full kernel's CTAs release
             const size_t wsl = strip_ws_bytes_per_warp_light(N);
             const int lw = strip_light_warps_per_cta();
             int64_t lctas = (int64_t)st->sm_count * st->light_occupancy;
             lctas = std::min<int64_t>(lctas, (queued + lw - 1) / lw);
-            lctas = std::min<int64_t>(lctas, (int64_t)(st->ws.bytes / (wsl * lw)));
-            if (lctas >= 1) {
-                StripLaunchArgs A;
-                A.in = in;
-                A.N = N;
-                A.out = out;
-                A.items = q_items;
-                A.item_lo = small + SM_HIST + 1;
-                A.n_items = q_count;
-                A.work_counter = small + SM_WORK;
-                A.ovf_items = ovf_items;
-                A.ovf_count = ovf_count;
-                A.vertex_sum = reinterpret_cast<unsigned long long*>(small + SM_VSUM);
-                A.ws = static_cast<char*>(st->ws.p);
-                A.ws_stride = wsl;
-                A.level = 0;
-                A.ctas = (int)lctas;
-                A.light = true;
-                if (strip_launch(A, s) != STATUS_OK) return cuda_fail(cudaGetLastError(), "light strip_kernel launch");
-                AMTC_CUDA(cudaMemsetAsync(small + SM_WORK, 0, sizeof(int), s));
+            const size_t full_b = wsb * wpc * (size_t)ctas;
+            lctas = std::min<int64_t>(lctas, (int64_t)((budget > full_b ? budget - full_b : 0) / (wsl * lw)));
+            if (lctas < 1) {
+                light_pass = false;
+            } else {
+                AMTC_CUDA(st->ws_light.ensure(wsl * lw * (size_t)lctas));
+                if (!st->s2) AMTC_CUDA(cudaStreamCreateWithFlags(&st->s2, cudaStreamNonBlocking));
+                if (!st->ev_fork) {
+                    AMTC_CUDA(cudaEventCreateWithFlags(&st->ev_fork, cudaEventDisableTiming));
+                    AMTC_CUDA(cudaEventCreateWithFlags(&st->ev_join, cudaEventDisableTiming));
+                }
+                AMTC_CUDA(cudaMemsetAsync(small + SM_WORK2, 0, sizeof(int), s));
+                AL.in = in;
+                AL.N = N;
+                AL.out = out;
+                AL.items = q_items;
+                AL.item_lo = small + SM_HIST + 1;
+                AL.n_items = q_count;
+                AL.work_counter = small + SM_WORK2;
+                AL.ovf_items = ovf_items;
+                AL.ovf_count = ovf_count;
+                AL.vertex_sum = reinterpret_cast<unsigned long long*>(small + SM_VSUM);
+                AL.ws = static_cast<char*>(st->ws_light.p);
+                AL.ws_stride = wsl;
+                AL.level = 0;
+                AL.ctas = (int)lctas;
+                AL.light = true;
             }
         }
         StripLaunchArgs A;
@@ -287,7 +301,14 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
         A.ws_stride = wsb;
         A.level = level;
         A.ctas = (int)ctas;
+        if (light_pass) AMTC_CUDA(cudaEventRecord(st->ev_fork, s));
         if (strip_launch(A, s) != STATUS_OK) return cuda_fail(cudaGetLastError(), "strip_kernel launch");
+        if (light_pass) {
+            AMTC_CUDA(cudaStreamWaitEvent(st->s2, st->ev_fork, 0));
+            if (strip_launch(AL, st->s2) != STATUS_OK) return cuda_fail(cudaGetLastError(), "light strip_kernel launch");
+            AMTC_CUDA(cudaEventRecord(st->ev_join, st->s2));
+            AMTC_CUDA(cudaStreamWaitEvent(s, st->ev_join, 0));
+        }
         AMTC_CUDA(cudaEventRecord(st->ev[2 * passes + 1], s));
         passes++;
         AMTC_CUDA(cudaMemcpyAsync(&ovf_host, ovf_count, sizeof(int), cudaMemcpyDeviceToHost, s));

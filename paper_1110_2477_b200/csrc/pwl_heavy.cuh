@@ -274,23 +274,27 @@ __device__ __forceinline__ void try_cross(const Line& A, const Line& B, double r
 
 // per-lane staging of output vertices (global scratch, lane-interleaved)
 struct Stage {
-    Vtx* buf;  // STAGE x 32
+    Vtx* buf;   // STAGE x 32 (global, lane-interleaved)
+    Vtx* sbuf;  // optional: rows 0 and 1 in shared memory (nullptr: all rows in buf)
     int lane, m, err;
     double last_s;  // slope after the last staged vertex
+    __device__ __forceinline__ Vtx& at(int q) const {
+        return (q < 2 && sbuf) ? sbuf[q * 32 + lane] : buf[q * 32 + lane];
+    }
     __device__ __forceinline__ void push(double x, double f, double s) {
         if (m > 0) {
-            Vtx& p = buf[(m - 1) * 32 + lane];
+            Vtx& p = at(m - 1);
             if (!(x > p.x + xtol(x))) {
                 // (near) zero-length piece: the previous vertex turns into slope s
                 // directly (reading A10, as pwl_device.cuh's Emit)
                 p.s = s;
-                if (m > 1 && buf[(m - 2) * 32 + lane].s == s) m--;  // no longer a kink
+                if (m > 1 && at(m - 2).s == s) m--;  // no longer a kink
                 last_s = s;
                 return;
             }
         }
         if (m >= STAGE) { err |= DEV_OVERFLOW; return; }
-        Vtx& o = buf[m * 32 + lane];
+        Vtx& o = at(m);
         o.x = x; o.f = f; o.s = s;
         m++;
         last_s = s;
@@ -465,6 +469,7 @@ __device__ __noinline__ int node_update_chunk(const Fn U, const Fn D, double lo,
         }
         Stage st;
         st.buf = stage_buf;
+        st.sbuf = nullptr;
         st.lane = lane;
         st.m = 0;
         st.err = DEV_OK;
@@ -903,6 +908,7 @@ struct HWin {
     Vtx u[33], d[33];  // [0]: the vertex before the window (or the left-tail anchor); [1..32]: window
     int ev[32];        // merged event k of the block: isU | idx << 1 | rank << 7
 };
+static_assert(sizeof(HWin) >= 2 * 32 * sizeof(Vtx), "sweep C stages two rows in the windows");
 
 __device__ __forceinline__ Vtx shfl_vtx(const Vtx& v, int src) {
     return Vtx{__shfl_sync(FULLM, v.x, src), __shfl_sync(FULLM, v.f, src), __shfl_sync(FULLM, v.s, src)};
@@ -1100,6 +1106,7 @@ __device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo,
         const bool first_overall = has && j == 0;
         Stage st;
         st.buf = stage_buf;
+        st.sbuf = reinterpret_cast<Vtx*>(&Wn);  // the merge windows are dead in sweep C: 2 stage rows
         st.lane = lane;
         st.m = 0;
         st.err = DEV_OK;
@@ -1160,14 +1167,14 @@ __device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo,
             const int lastv = min(31, nW - 1 - blk * 32);
             s_in = __shfl_sync(FULLM, s_end, lastv);
         }
-        const int skip0 = (pending && stage_buf[lane].s == s_left) ? 1 : 0;
+        const int skip0 = (pending && st.at(0).s == s_left) ? 1 : 0;
         if (__reduce_or_sync(FULLM, st.err)) { err = DEV_FALLBACK; break; }  // stage overflow
         int cnt = st.m - skip0;
         double f0x = 0.0, fs = 0.0, lx = -INFINITY;
         if (cnt > 0) {
-            f0x = stage_buf[skip0 * 32 + lane].x;
-            fs = stage_buf[skip0 * 32 + lane].s;
-            lx = stage_buf[(st.m - 1) * 32 + lane].x;
+            f0x = st.at(skip0).x;
+            fs = st.at(skip0).s;
+            lx = st.at(st.m - 1).x;
         }
         int prevl = cnt > 0 ? lane : -1;
         int nextl = cnt > 0 ? lane : 32;
@@ -1187,7 +1194,7 @@ __device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo,
         const bool fold = cnt > 0 && !(f0x > prev_x + xtol(f0x));
         const int nfold = __shfl_sync(FULLM, (int)fold, nl > 31 ? 0 : nl);
         const double nfs = __shfl_sync(FULLM, fs, nl > 31 ? 0 : nl);
-        if (cnt > 0 && nl <= 31 && nfold) stage_buf[(st.m - 1) * 32 + lane].s = nfs;
+        if (cnt > 0 && nl <= 31 && nfold) st.at(st.m - 1).s = nfs;
         if (fold && pl < 0 && total > 0) arena[base + total - 1].s = fs;
         const int drop_first = (fold && (pl >= 0 || total > 0)) ? 1 : 0;
         cnt -= drop_first;
@@ -1195,7 +1202,7 @@ __device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo,
         const int off = excl_prefix_sum(cnt, lane, tot);
         if (base + total + tot > acap) { err = DEV_OVERFLOW; break; }
         for (int q = 0; q < cnt; ++q)
-            arena[base + total + off + q] = stage_buf[(q + skip0 + drop_first) * 32 + lane];
+            arena[base + total + off + q] = st.at(q + skip0 + drop_first);
         total += tot;
         {
             const int lastl = __shfl_sync(FULLM, prevl, 31);

@@ -5,6 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_1110_2477_b200 import api, build, workloads as W
 build.build(); api.lib()
+if os.environ.get("AMTC_LIGHT") == "0": api.debug_set_light_kernel(False)
 kind = sys.argv[1]; n = int(sys.argv[2]); N = int(sys.argv[3])
 b = W.config4()
 idx = np.arange(len(b)) if kind == "all" else np.nonzero(b.kind == int(kind))[0]
