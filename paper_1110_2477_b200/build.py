@@ -27,6 +27,8 @@ NCCL = _nccl_dir()
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", os.path.join(NCCL, "include")]
+# developer experiments: extra nvcc flags (e.g. -DAMTC_LIGHT_CFG=6,6,8,3)
+FLAGS += os.environ.get("AMTC_NVCC_EXTRA", "").split()
 LINK = ["-L", os.path.join(NCCL, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath," + os.path.join(NCCL, "lib")]
 
 

@@ -615,11 +615,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
 // every put buyer: DESIGN.md section 5); a heavy node there aborts the item,
 // which the full kernel re-runs.
 constexpr int STRIP_C = 6, STRIP_B = 6, STRIP_WARPS = 16, STRIP_MINB = 1;
-constexpr int LIGHT_WARPS = 8, LIGHT_MINB = 3;
+#ifndef AMTC_LIGHT_CFG
+#define AMTC_LIGHT_CFG 6, 6, 8, 3
+#endif
+constexpr int LIGHT_CFG[4] = {AMTC_LIGHT_CFG};
+constexpr int LIGHT_C = LIGHT_CFG[0], LIGHT_B = LIGHT_CFG[1], LIGHT_WARPS = LIGHT_CFG[2], LIGHT_MINB = LIGHT_CFG[3];
 #define STRIP_KERNEL strip_kernel<STRIP_C, STRIP_B, STRIP_WARPS, STRIP_MINB, true>
-#define LIGHT_KERNEL strip_kernel<STRIP_C, STRIP_B, LIGHT_WARPS, LIGHT_MINB, false>
+#define LIGHT_KERNEL strip_kernel<LIGHT_C, LIGHT_B, LIGHT_WARPS, LIGHT_MINB, false>
 constexpr size_t STRIP_SMEM = sizeof(CtaHdr) + sizeof(StripSmem<STRIP_C, STRIP_B, true>) * STRIP_WARPS;
-constexpr size_t LIGHT_SMEM = sizeof(CtaHdr) + sizeof(StripSmem<STRIP_C, STRIP_B, false>) * LIGHT_WARPS;
+constexpr size_t LIGHT_SMEM = sizeof(CtaHdr) + sizeof(StripSmem<LIGHT_C, LIGHT_B, false>) * LIGHT_WARPS;
 
 static int strip_set_smem() {
     static int done = 0;
@@ -663,6 +667,8 @@ StripCaps strip_caps(int N, int level) {
 // the light kernel: no tier 3, small arenas (its functions stay below ~10 vertices)
 static StripCaps strip_caps_light(int N) {
     StripCaps c = strip_caps(N, 0);
+    c.C = LIGHT_C;
+    c.B = LIGHT_B;
     c.rarena_cap = 8 * (N + 2) + 4096;
     c.carena_cap = 8 * (N + 2) + 4096;
     c.hscr_cap = 0;

@@ -2,7 +2,7 @@
 
 Calls ONLY oracle/ (and the seeded generators in paper_1110_2477_b200/workloads.py,
 which hold none of the method's arithmetic).  Never reads the CUDA path.
-Usage: python scripts/make_oracle_refs.py [config3|config4|config2|all]
+Usage: python scripts/make_oracle_refs.py [config2|config3|config4|config5b|all]
 """
 import json
 import os
@@ -74,9 +74,18 @@ def config2(n_sample=256, seed=11):
             "N": W.CONFIG2_N, "samples": res}
 
 
+def config5b():
+    r = W.config5b().row(0)
+    t = time.time()
+    q = O.price_tc(opt(r), W.CONFIG5B_N)
+    return {"_source": "oracle/amtc_oracle.c via scripts/make_oracle_refs.py (BASELINE.json config 5b)",
+            "N": W.CONFIG5B_N, "ask": q.ask, "bid": q.bid, "status": q.status,
+            "max_kinks": max(q.max_kinks_ask, q.max_kinks_bid), "seconds": time.time() - t}
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
-    for name, fn in (("config2", config2), ("config4", config4), ("config3", config3)):
+    for name, fn in (("config2", config2), ("config4", config4), ("config3", config3), ("config5b", config5b)):
         if what not in (name, "all"):
             continue
         t = time.time()
