@@ -260,3 +260,13 @@ def test_light_kernel_matches_full_kernel(api):
     np.testing.assert_allclose(got["ask"], ref["ask"], rtol=1e-12, atol=1e-12)
     np.testing.assert_allclose(got["bid"], ref["bid"], rtol=1e-12, atol=1e-12)
     assert_quotes(got, b, N)
+
+
+def test_config5b_full_size_golden(api):
+    """BASELINE config 5b at full size (N=8000, k=0.005) through the north-star
+    call (split mode), against the stored oracle value (scripts/make_oracle_refs.py)."""
+    ref = json.load(open(os.path.join(GOLD, "oracle_config5b.json")))
+    r = W.config5b().row(0)
+    q = api.price_american_tc(r["S0"], r["K"], r["T"], r["sigma"], r["R"], ref["N"], r["k"], api.PUT)
+    assert q["status"] == 0
+    assert close(q["ask"], ref["ask"]) and close(q["bid"], ref["bid"]), (q, ref)
