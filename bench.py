@@ -375,14 +375,24 @@ def run_tree(args):
             desc = "config1: Example 5.1 put, N=100, ask+bid (north-star single call)"
         else:
             trees = [(b.row(0), N_) for b, N_ in W.config3()]
-            desc = "config3: put+call x k in {0,.0025,.005,.01,.02} x N in {250..2000}, 50 single trees"
+            desc = ("config3: put+call x k in {0,.0025,.005,.01,.02} x N in {250..2000}, 50 single trees, "
+                    "one batched call per N (10 trees, strip-split mode: intra-tree parallel)")
+        groups = {}
+        for b, N_ in ([(W.config1(), W.CONFIG1_N)] if args.config == 1 else W.config3()):
+            groups.setdefault(N_, []).append(b)
+        batches = {N_: W.concat(bs) for N_, bs in groups.items()}
         def step():
             if rank != 0:
                 return
-            for row, N_ in trees:
+            if args.config == 1:
+                row, N_ = trees[0]
                 q = api.price_american_tc(row["S0"], row["K"], row["T"], row["sigma"], row["R"], N_, row["k"],
                                           row["kind"], row["K2"])
                 assert q["status"] == 0, q
+                return
+            for N_, bb in batches.items():
+                q, rc = api.price_american_tc_batch_host(bb, N_)
+                assert rc == 0, rc
         nodes = sum(tc_nodes(N_) for _, N_ in trees)
         scaling = "weak"
         row0, N0 = trees[0]

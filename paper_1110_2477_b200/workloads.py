@@ -48,6 +48,11 @@ class Batch:
                 for f in self.fields()}
 
 
+def concat(batches) -> Batch:
+    """Concatenate batches (e.g. the single-tree points of one N)."""
+    return Batch(*(np.concatenate([getattr(b, f) for b in batches]) for f in Batch.fields()))
+
+
 def _batch(S0, K, K2, T, sigma, R, k, kind) -> Batch:
     n = len(K)
     f = lambda a: np.array(np.broadcast_to(np.asarray(a, dtype=np.float64), (n,)), copy=True)

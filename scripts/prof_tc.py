@@ -6,6 +6,7 @@ import numpy as np, torch
 from paper_1110_2477_b200 import api, build, workloads as W
 build.build(); api.lib()
 if os.environ.get("AMTC_LIGHT") == "0": api.debug_set_light_kernel(False)
+if os.environ.get("AMTC_SPLIT") is not None: api.debug_set_split_mode(int(os.environ["AMTC_SPLIT"]))
 kind = sys.argv[1]; n = int(sys.argv[2]); N = int(sys.argv[3])
 b = W.config4()
 idx = np.arange(len(b)) if kind == "all" else np.nonzero(b.kind == int(kind))[0]
