@@ -1,8 +1,14 @@
 // pwl_heavy.cuh -- warp-cooperative node update for HEAVY node functions (the
 // buyer's "sawtooth" of calls / bull spreads: thousands of vertices, DESIGN.md
-// "Breakpoint counts").  Chunk-synchronous: the merged vertex sequence of the
-// two children is cut into blocks of 32 events and lane i owns event 32 b + i,
-// so loads are coalesced and all lanes do the same work.
+// section 5).  Three implementations of the same data-parallel form:
+//   node_update_block  (default, tier 3) block-synchronous: merged events in
+//                      blocks of 32 from shared merge windows (ranks by binary
+//                      search in shared memory), W compacted to scratch, then
+//                      per-W-vertex emission of z; no dependent global loads.
+//   node_update        (fallback for rare shapes) lane-contiguous: lane i runs
+//                      the sequential generator over 1/32 of the events.
+//   node_update_chunk  (fallback of the fallback) chunk-synchronous with merge-
+//                      path binary searches in global memory.
 //
 // Data-parallel form of one node (Sec. 3; reading A7): with
 //   W = max(U, D)                              (discounted, so no /r)
@@ -12,17 +18,12 @@
 //   v(y) = min( W(y), lo y + M_{j+1}, hi y + P_j )
 // (the infimum of a piecewise-linear function over a half line is attained at
 // its end point or at a vertex; the tails are monotone when d < r < u), and
-// z = max(u, v) (seller) / min(u, v) (buyer).
-// Sweep 1 (right to left) stores, per block, the suffix minimum of g and the
-// first vertex of W to its right; sweep 2 (left to right) rebuilds W, scans M
-// and P inside the block, and the lane owning W vertex j emits z's vertices on
-// [x_j, x_{j+1}).  Vertices are staged per lane, de-duplicated against the
-// slope arriving from the left, and compacted with a warp prefix sum.
+// z = max(u, v) (seller) / min(u, v) (buyer).  The vertex owner
+// of piece j emits z's vertices on [x_j, x_{j+1}); vertices are staged per lane,
+// de-duplicated against the slope arriving from the left, folded when closer
+// than xtol (reading A10) and compacted with a warp prefix sum.
 #pragma once
 #include "pwl_device.cuh"
-#ifdef HEAVY_STATS
-extern long g_stat[8];
-#endif
 
 namespace amtc {
 namespace heavy {
@@ -1128,35 +1129,13 @@ __device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo,
             const double Pj = fmin(Pl, hl);
             const Line LWr{wv.x, wv.f, wv.s}, LMr{0.0, Mnext, lo}, LPr{0.0, Pj, hi};
             const double sr_ = z_side(LWr, LMr, isfinite(Mnext), LPr, true, c, wv.x, true, vi, zU, zv);
-#ifdef HEAVY_STATS
-            {
-                
-                const int m0 = st.m;
-                const double sr2 = sr_;
-                (void)sr2;
-                g_stat[0]++;
-                if (wv.s >= lo && wv.s <= hi) g_stat[1]++;
-                if (vi == 0 && !zU) g_stat[2]++;
-                (void)m0;
-            }
-#endif
             if (s_run != s_run) {
                 pending = st.m == 0;
                 st.push(wv.x, zv, sr_);
             } else if (sr_ != s_run) {
                 st.push(wv.x, zv, sr_);
             }
-#ifdef HEAVY_STATS
-            const int m1 = st.m;
-#endif
             s_run = emit_open(wv.x, xn, LWr, LMr, isfinite(Mnext), LPr, true, c, sr_, false, st);
-#ifdef HEAVY_STATS
-            {
-                
-                if (st.m == m1) g_stat[3]++;
-                if (st.m == m1 && vi == 0 && !zU) g_stat[4]++;
-            }
-#endif
         }
         const double s_end = s_run;
         // the slope arriving from the left: s_end of the previous lane (all lanes

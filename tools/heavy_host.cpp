@@ -4,7 +4,6 @@
 // stdin: "S0 K K2 T sigma R k kind N" per line; stdout per line:
 //   "<nodes> <max vertex excess> <max rel value diff> <status>"
 #include "warp_emu.h"
-long g_stat[8];
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
@@ -108,7 +107,6 @@ int main(int argc, char** argv) {
             }
         }
         std::printf("%ld %d %.3g %d\n", nodes, worst_excess, worst_rel, status);
-        if (std::getenv("HEAVY_STATS_PRINT")) std::fprintf(stderr, "pieces %ld inband %ld W-active-notU %ld no-emit %ld no-emit-and-trivialstart %ld\n", g_stat[0], g_stat[1], g_stat[2], g_stat[3], g_stat[4]);
         std::fflush(stdout);
     }
     return 0;
