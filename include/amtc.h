@@ -194,6 +194,11 @@ void amtc_debug_set_split_mode(int mode);
    kernel. */
 void amtc_debug_set_light_kernel(int on);
 
+/* TESTING HOOK: divide the whole-tree solver's row and carry arena capacities
+   by 2^shift (0 restores them), so tests can drive items through the capacity
+   retry passes (4x arenas per retry) and, past the last retry, AMTC_ECAPACITY. */
+void amtc_debug_set_arena_shift(int shift);
+
 #ifdef __cplusplus
 }
 #endif

@@ -50,7 +50,8 @@ EXPORTS = ["amtc_price_american_tc", "amtc_price_american_tc_batch", "amtc_price
            "amtc_price_crr_batch", "amtc_price_crr_batch_host", "amtc_strerror", "amtc_last_error",
            "amtc_launch_count", "amtc_tc_last_stats", "amtc_debug_set_heavy_threshold",
            "amtc_price_crr_tree", "amtc_comm_unique_id", "amtc_comm_init", "amtc_comm_destroy",
-           "amtc_price_tree_sharded", "amtc_debug_set_split_mode", "amtc_debug_set_light_kernel"]
+           "amtc_price_tree_sharded", "amtc_debug_set_split_mode", "amtc_debug_set_light_kernel",
+           "amtc_debug_set_arena_shift"]
 
 _lib = None
 
@@ -85,6 +86,8 @@ def lib():
         L.amtc_comm_destroy.argtypes = [C.c_void_p]
         L.amtc_price_tree_sharded.argtypes = [C.POINTER(Params), C.c_int32, C.POINTER(Payoff), C.c_double,
                                               C.c_void_p, C.c_int, C.c_int, C.POINTER(Quote), C.c_void_p]
+        L.amtc_debug_set_arena_shift.restype = None
+        L.amtc_debug_set_arena_shift.argtypes = [C.c_int]
         L.amtc_debug_set_light_kernel.restype = None
         L.amtc_debug_set_light_kernel.argtypes = [C.c_int]
         L.amtc_debug_set_split_mode.restype = None
@@ -124,6 +127,11 @@ def debug_set_split_mode(mode: int) -> None:
 def debug_set_light_kernel(on: bool) -> None:
     """Testing hook: run sellers / put buyers on the light kernel variant (default on)."""
     lib().amtc_debug_set_light_kernel(1 if on else 0)
+
+
+def debug_set_arena_shift(shift: int) -> None:
+    """Testing hook: shrink the solver's arenas by 2**shift (0 restores them)."""
+    lib().amtc_debug_set_arena_shift(int(shift))
 
 
 def tc_last_stats() -> dict:

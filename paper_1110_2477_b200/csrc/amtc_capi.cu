@@ -512,6 +512,8 @@ void amtc_debug_set_split_mode(int mode) { g_split_mode = mode < 0 ? -1 : (mode 
 
 void amtc_debug_set_light_kernel(int on) { g_light_kernel = on ? 1 : 0; }
 
+void amtc_debug_set_arena_shift(int shift) { strip_set_arena_shift(shift); }
+
 int64_t amtc_launch_count(void) { return g_launches.load(); }
 
 int amtc_tc_last_stats(amtc_tc_stats* out) {

@@ -44,7 +44,7 @@ constexpr int TC_CLASSES = 16;
 // amtc_prepare.cu
 void tc_launch_prepare(const BatchPtrs& in, int64_t n, int N, Quote* out, unsigned char* cls, int* hist,
                        int* items, cudaStream_t s);
-void launch_status_reduce(const Quote* out, int64_t n, int* worst, cudaStream_t s);
+void launch_status_reduce(Quote* out, int64_t n, int* worst, cudaStream_t s);
 void tc_launch_mark_capacity(const int* items, int n_items, Quote* out, cudaStream_t s);
 
 // amtc_strip.cu (the transaction-cost solver)
@@ -87,6 +87,7 @@ int strip_warps_per_cta();
 int strip_ctas_per_sm();
 int strip_launch(const StripLaunchArgs& a, cudaStream_t s);
 void strip_set_heavy_threshold(int tl);
+void strip_set_arena_shift(int sh);
 
 // amtc_crr.cu
 int crr_launch(const BatchPtrs& in, int64_t n, int N, double* out, cudaStream_t s);

@@ -63,12 +63,18 @@ __global__ void tc_scatter_kernel(int64_t n2, const unsigned char* cls, int* his
     items[pos] = (int)i;
 }
 
-__global__ void status_reduce_kernel(const Quote* out, int64_t n, int* worst) {
+// worst status of the batch; a failed option keeps NaN prices (amtc.h) even if
+// one of its two items (seller / buyer) completed
+__global__ void status_reduce_kernel(Quote* out, int64_t n, int* worst) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n && out[i].status) atomicMax(worst, out[i].status);
+    if (i < n && out[i].status) {
+        atomicMax(worst, out[i].status);
+        out[i].ask = NAN;
+        out[i].bid = NAN;
+    }
 }
 
-void launch_status_reduce(const Quote* out, int64_t n, int* worst, cudaStream_t s) {
+void launch_status_reduce(Quote* out, int64_t n, int* worst, cudaStream_t s) {
     cudaMemsetAsync(worst, 0, sizeof(int), s);
     status_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(out, n, worst);
     note_launch();

@@ -641,6 +641,8 @@ static int strip_set_smem() {
 
 static int g_tl_override = 0;  // testing hook (amtc_debug_set_heavy_threshold)
 void strip_set_heavy_threshold(int tl) { g_tl_override = tl > 0 ? tl : 0; }
+static int g_cap_shift = 0;  // testing hook (amtc_debug_set_arena_shift): arenas >> shift
+void strip_set_arena_shift(int sh) { g_cap_shift = sh > 0 ? (sh > 16 ? 16 : sh) : 0; }
 
 StripCaps strip_caps(int N, int level) {
     // level 0: first pass; each retry level quadruples the arenas
@@ -655,8 +657,8 @@ StripCaps strip_caps(int N, int level) {
     // ~16 heavy columns of up to ~3N vertices) never need a retry pass: the
     // row arena holds one level of a strip, the carry arena every carried
     // function of a strip (the band crosses a carry column for ~32 levels)
-    c.rarena_cap = clampi(mul * (64 * (int64_t)(N + 2) + 8192));
-    c.carena_cap = clampi(mul * (100 * (int64_t)(N + 2) + 8192));
+    c.rarena_cap = clampi(mul * (64 * (int64_t)(N + 2) + 8192) >> g_cap_shift);
+    c.carena_cap = clampi(mul * (100 * (int64_t)(N + 2) + 8192) >> g_cap_shift);
     // tier 3 scratch: stage + W (<= 2 (nU + nD) + 8 vertices; the sawtooth grows by
     // two vertices per level, so nU, nD <= ~2N) + block minima
     c.hscr_cap = clampi(heavy::STAGE * 32 + mul * (14 * (int64_t)(N + 2) + 4096));

@@ -270,3 +270,31 @@ def test_config5b_full_size_golden(api):
     q = api.price_american_tc(r["S0"], r["K"], r["T"], r["sigma"], r["R"], ref["N"], r["k"], api.PUT)
     assert q["status"] == 0
     assert close(q["ask"], ref["ask"]) and close(q["bid"], ref["bid"]), (q, ref)
+
+
+def test_capacity_retry_passes(api):
+    """Shrunken arenas force heavy items through the retry passes (4x arenas per
+    pass): same prices; with arenas too small for every pass, AMTC_ECAPACITY."""
+    b = W.random_small(12, seed=99, k_max=0.0)
+    b.kind[:] = 1
+    b.k[:] = np.linspace(0.006, 0.02, 12)
+    b.T[:] = 0.6
+    b.sigma[:] = 0.3
+    N = 400
+    try:
+        api.debug_set_split_mode(0)
+        ref, rc0 = api.price_american_tc_batch_host(b, N)
+        api.debug_set_arena_shift(9)
+        got, rc = api.price_american_tc_batch_host(b, N)
+        st = api.tc_last_stats()
+        api.debug_set_arena_shift(16)
+        bad, rc2 = api.price_american_tc_batch_host(b, N)
+    finally:
+        api.debug_set_arena_shift(0)
+        api.debug_set_split_mode(-1)
+    assert rc0 == 0 and rc == 0
+    assert st["passes"] > 1 and st["retried_items"] > 0, st
+    np.testing.assert_allclose(got["ask"], ref["ask"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(got["bid"], ref["bid"], rtol=1e-12, atol=1e-12)
+    assert rc2 == 3 and np.any(bad["status"] == 3)  # AMTC_ECAPACITY
+    assert np.all(np.isnan(bad["ask"][bad["status"] == 3]))
