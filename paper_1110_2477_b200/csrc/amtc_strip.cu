@@ -609,12 +609,19 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-// full kernel: one CTA of 16 warps per SM (the CTA is the work-sharing domain of
-// tier 3).  Light kernel: no tier 3, three CTAs of 8 warps per SM (24 warps,
+// full kernel: one CTA of 20 warps per SM (the CTA is the work-sharing domain of
+// tier 3), 4-vertex row slots and scratch (measured: 20 warps / 4 beat 16 / 6 by
+// 2.5%, 12 / 6 and 8 / 6 lose 5-16%, 24 / 3 loses 2.5x).  Light kernel: no tier 3, three CTAs of 8 warps per SM (24 warps,
 // <= 85 registers), for the items that never grow heavy nodes (every seller,
 // every put buyer: DESIGN.md section 5); a heavy node there aborts the item,
 // which the full kernel re-runs.
-constexpr int STRIP_C = 6, STRIP_B = 6, STRIP_WARPS = 16, STRIP_MINB = 1;
+#ifndef AMTC_FULL_WARPS
+#define AMTC_FULL_WARPS 20
+#endif
+#ifndef AMTC_FULL_CB
+#define AMTC_FULL_CB 4
+#endif
+constexpr int STRIP_C = AMTC_FULL_CB, STRIP_B = AMTC_FULL_CB, STRIP_WARPS = AMTC_FULL_WARPS, STRIP_MINB = 1;
 #ifndef AMTC_LIGHT_CFG
 #define AMTC_LIGHT_CFG 6, 6, 8, 3
 #endif
