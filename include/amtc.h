@@ -145,14 +145,25 @@ int amtc_comm_destroy(void* comm);
  * g owns columns [ceil(g w/n), ceil((g+1) w/n)) of the current level (w = t+1),
  * re-split every band of 128 levels (the paper's per-round rebalancing,
  * P:178); before each band the ranks exchange their window halos with
- * ncclSend/ncclRecv (region-B dependency).  Every rank receives the
- * quote in *out (HOST pointer).  k = 0 only for nranks > 1 (the transaction-
- * cost tree is not sharded yet: AMTC_EINVAL); with nranks = 1 and k > 0 this
- * is amtc_price_american_tc.  nccl_comm may be NULL when nranks = 1.
+ * ncclSend/ncclRecv (region-B dependency).  k > 0: the tree's
+ * 32-column strips (strip-split mode of the transaction-cost solver) are
+ * partitioned into contiguous ranges of equal work; the only cross-GPU
+ * dependency is the carry column of each range's first strip, which the left
+ * neighbour's kernel reads from the owner's memory through CUDA IPC (handles
+ * all-gathered over the communicator) while polling the owner's per-level
+ * progress counter (published with system-scope fences).  Every rank receives
+ * the quote in *out (HOST pointer).  nccl_comm may be NULL when nranks = 1
+ * (then k > 0 is amtc_price_american_tc); trees with N < 64 are not sharded.
  * Synchronous on cuda_stream.  Returns the status (also in out->status).
  */
 int amtc_price_tree_sharded(const amtc_params* params, int32_t N, const amtc_payoff* payoff, double k,
                             void* nccl_comm, int rank, int nranks, amtc_quote* out, void* cuda_stream);
+
+/* Host-only helper (no GPU needed): the strip partition amtc_price_tree_sharded
+   uses for k > 0 -- rank g owns the 32-column strips [lo[g], lo[g+1]) of the
+   N-step tree (N/32 + 1 strips, strip s carrying N - 32 s + 1 levels), ranges of
+   equal work, rank 0 holding strip 0 (the root).  lo: nranks + 1 ints. */
+int amtc_tree_shard_plan(int32_t N, int nranks, int32_t* lo);
 
 /* Human-readable name of a status code (static storage). */
 const char* amtc_strerror(int status);

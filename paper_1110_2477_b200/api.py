@@ -51,7 +51,7 @@ EXPORTS = ["amtc_price_american_tc", "amtc_price_american_tc_batch", "amtc_price
            "amtc_launch_count", "amtc_tc_last_stats", "amtc_debug_set_heavy_threshold",
            "amtc_price_crr_tree", "amtc_comm_unique_id", "amtc_comm_init", "amtc_comm_destroy",
            "amtc_price_tree_sharded", "amtc_debug_set_split_mode", "amtc_debug_set_light_kernel",
-           "amtc_debug_set_arena_shift"]
+           "amtc_debug_set_arena_shift", "amtc_tree_shard_plan"]
 
 _lib = None
 
@@ -86,6 +86,7 @@ def lib():
         L.amtc_comm_destroy.argtypes = [C.c_void_p]
         L.amtc_price_tree_sharded.argtypes = [C.POINTER(Params), C.c_int32, C.POINTER(Payoff), C.c_double,
                                               C.c_void_p, C.c_int, C.c_int, C.POINTER(Quote), C.c_void_p]
+        L.amtc_tree_shard_plan.argtypes = [C.c_int32, C.c_int, C.POINTER(C.c_int32)]
         L.amtc_debug_set_arena_shift.restype = None
         L.amtc_debug_set_arena_shift.argtypes = [C.c_int]
         L.amtc_debug_set_light_kernel.restype = None
@@ -302,3 +303,12 @@ def price_tree_sharded(S0: float, K: float, T: float, sigma: float, R: float, N:
     rc = lib().amtc_price_tree_sharded(C.byref(p), N, C.byref(y), k, comm, rank, nranks, C.byref(q),
                                        _stream_handle(stream))
     return {"ask": q.ask, "bid": q.bid, "status": q.status if rc == q.status else rc, "max_bp": q.max_bp}
+
+
+def tree_shard_plan(N: int, nranks: int) -> list:
+    """Strip partition of the sharded transaction-cost tree (host only)."""
+    lo = (C.c_int32 * (nranks + 1))()
+    rc = lib().amtc_tree_shard_plan(N, nranks, lo)
+    if rc:
+        raise ValueError(f"amtc_tree_shard_plan: {STATUS.get(rc, rc)}")
+    return list(lo)

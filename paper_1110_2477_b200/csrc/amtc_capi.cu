@@ -6,6 +6,7 @@
 // bounds and fewer resident CTAs), and marshals host buffers for the *_host
 // variants.  No exception crosses the boundary.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
@@ -57,6 +58,7 @@ struct DevState {
     DevBuf items[2], cls, small, ws, stage_in, stage_out;
     DevBuf sp_items, sp_progress, sp_carry, sp_arena, sp_cnt;  // split mode
     DevBuf ws_light;                                          // light-kernel workspaces
+    DevBuf ipc;                                               // IPC handle exchange
     cudaStream_t s2 = nullptr;                                // light-kernel stream
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     size_t budget = 0;  // cached workspace budget (bytes)
@@ -340,6 +342,189 @@ finish:
     return worst;
 }
 
+// ---------------------------------------------------------------------------
+// One transaction-cost tree sharded over the GPUs of an NCCL communicator
+// (SURVEY 8(e), config 5b).  The tree's strips (split mode) are partitioned
+// into contiguous ranges of equal work (strip s has N - 32 s + 1 levels); rank
+// g owns [lo_g, hi_g), rank 0 the root strip.  The only cross-GPU dependency is
+// the carry column of strip hi_g (the first strip of rank g+1), read by rank
+// g's strip hi_g - 1 at every level: rank g maps rank g+1's carry, carry-arena
+// and progress buffers through CUDA IPC (handles all-gathered over NCCL) and
+// its kernel reads them over NVLink, waiting on the peer's progress counter,
+// which the producer publishes with system-scope fences.  NCCL collectives
+// before and after the launch order the buffer resets and the reuse.
+// ---------------------------------------------------------------------------
+static int nccl_fail(ncclResult_t r, const char* what) {
+    g_last_error = std::string(what) + ": " + ncclGetErrorString(r);
+    return STATUS_ENCCL;
+}
+#define AMTC_NCCL(call)                                   \
+    do {                                                  \
+        ncclResult_t r_ = (call);                         \
+        if (r_ != ncclSuccess) return nccl_fail(r_, #call); \
+    } while (0)
+
+// strip ranges of equal work: strip s carries N - 32 s + 1 levels
+static void shard_strips(int N, int nranks, std::vector<int>& lo) {
+    const int S = N / 32 + 1;
+    std::vector<double> cum(S + 1, 0.0);
+    for (int s = 0; s < S; ++s) cum[s + 1] = cum[s] + (double)(N - 32 * s + 1);
+    lo.assign(nranks + 1, S);
+    lo[0] = 0;
+    int s = 0;
+    for (int g = 1; g < nranks; ++g) {
+        const double target = cum[S] * g / nranks;
+        while (s < S && cum[s] < target) ++s;
+        lo[g] = std::max(s, lo[g - 1]);
+    }
+    lo[nranks] = S;
+}
+
+static size_t soa_bytes(int64_t n);
+static int stage_in(DevState* st, const amtc_batch_soa* h, int64_t n, amtc_batch_soa* d, cudaStream_t s);
+
+int tc_tree_sharded(const void* params_v, int N, const void* payoff_v, double k, void* comm_v, int rank, int nranks,
+                    void* out_v, cudaStream_t s) {
+    const amtc_params* p = static_cast<const amtc_params*>(params_v);
+    const amtc_payoff* y = static_cast<const amtc_payoff*>(payoff_v);
+    amtc_quote* out = static_cast<amtc_quote*>(out_v);
+    ncclComm_t comm = static_cast<ncclComm_t>(comm_v);
+    if (N < 64) return STATUS_EINVAL;  // fewer than three strips: nothing to shard
+    int dev = 0;
+    AMTC_CUDA(cudaGetDevice(&dev));
+    DevState* st = state_for_device(dev);
+    // one option, host -> device
+    double S0 = p->S0, K = y->K, K2 = y->K2, T = p->T, sg = p->sigma, R = p->R, kk = k;
+    int32_t kind = y->kind;
+    amtc_batch_soa h;
+    h.S0 = &S0; h.K = &K; h.K2 = &K2; h.T = &T; h.sigma = &sg; h.R = &R; h.k = &kk; h.kind = &kind;
+    std::lock_guard<std::mutex> guard(st->mu);
+    if (!st->sm_count) {
+        AMTC_CUDA(cudaDeviceGetAttribute(&st->sm_count, cudaDevAttrMultiProcessorCount, dev));
+        st->occupancy = strip_ctas_per_sm();
+        st->light_occupancy = strip_light_ctas_per_sm();
+    }
+    amtc_batch_soa d;
+    int rc = stage_in(st, &h, 1, &d, s);
+    if (rc) return rc;
+    BatchPtrs in = to_ptrs(&d);
+    AMTC_CUDA(st->stage_out.ensure(sizeof(amtc_quote)));
+    Quote* dq = static_cast<Quote*>(st->stage_out.p);
+    AMTC_CUDA(st->items[0].ensure(sizeof(int) * 2));
+    AMTC_CUDA(st->cls.ensure(2));
+    AMTC_CUDA(st->small.ensure(sizeof(int) * SM_INTS));
+    int* small = static_cast<int*>(st->small.p);
+    tc_launch_prepare(in, 1, N, dq, static_cast<unsigned char*>(st->cls.p), small + SM_HIST,
+                      static_cast<int*>(st->items[0].p), s);
+    AMTC_CUDA(cudaMemsetAsync(small + SM_VSUM, 0, sizeof(unsigned long long), s));
+    // split-mode buffers for both trees (seller, buyer) over ALL strips (IPC-mapped by rank-1)
+    const int S = N / 32 + 1;
+    const int64_t nsp = 2 * (int64_t)S;
+    const size_t carry_b = strip_carry_bytes(N);
+    const int acap = strip_split_arena_cap(N);
+    AMTC_CUDA(st->sp_items.ensure(sizeof(int) * (size_t)nsp));
+    AMTC_CUDA(st->sp_progress.ensure(sizeof(int) * (size_t)nsp));
+    AMTC_CUDA(st->sp_carry.ensure(carry_b * (size_t)nsp));
+    AMTC_CUDA(st->sp_arena.ensure((size_t)2 * acap * strip_vtx_bytes()));
+    AMTC_CUDA(st->sp_cnt.ensure(sizeof(int) * 2));
+    AMTC_CUDA(cudaMemsetAsync(st->sp_progress.p, 0x7f, sizeof(int) * (size_t)nsp, s));
+    AMTC_CUDA(cudaMemsetAsync(st->sp_cnt.p, 0, sizeof(int) * 2, s));
+    std::vector<int> lo;
+    shard_strips(N, nranks, lo);
+    const int s_lo = lo[rank], s_hi = lo[rank + 1];
+    // exchange IPC handles of (carry, arena, progress); map rank+1's
+    char* peer_carry = nullptr;
+    void* peer_arena = nullptr;
+    int* peer_prog = nullptr;
+    if (nranks > 1) {
+        cudaIpcMemHandle_t mine[3];
+        AMTC_CUDA(cudaIpcGetMemHandle(&mine[0], st->sp_carry.p));
+        AMTC_CUDA(cudaIpcGetMemHandle(&mine[1], st->sp_arena.p));
+        AMTC_CUDA(cudaIpcGetMemHandle(&mine[2], st->sp_progress.p));
+        const size_t hb = sizeof(mine);
+        AMTC_CUDA(st->ipc.ensure(hb * (size_t)(nranks + 1)));
+        char* dh = static_cast<char*>(st->ipc.p);
+        AMTC_CUDA(cudaMemcpyAsync(dh + hb * nranks, mine, hb, cudaMemcpyHostToDevice, s));
+        AMTC_NCCL(ncclAllGather(dh + hb * nranks, dh, hb, ncclUint8, comm, s));
+        std::vector<char> all(hb * nranks);
+        AMTC_CUDA(cudaMemcpyAsync(all.data(), dh, hb * nranks, cudaMemcpyDeviceToHost, s));
+        AMTC_CUDA(cudaStreamSynchronize(s));
+        if (rank + 1 < nranks) {
+            cudaIpcMemHandle_t peer[3];
+            std::memcpy(peer, all.data() + hb * (rank + 1), hb);
+            void* pc = nullptr;
+            void* pa = nullptr;
+            void* pp = nullptr;
+            AMTC_CUDA(cudaIpcOpenMemHandle(&pc, peer[0], cudaIpcMemLazyEnablePeerAccess));
+            AMTC_CUDA(cudaIpcOpenMemHandle(&pa, peer[1], cudaIpcMemLazyEnablePeerAccess));
+            AMTC_CUDA(cudaIpcOpenMemHandle(&pp, peer[2], cudaIpcMemLazyEnablePeerAccess));
+            peer_carry = static_cast<char*>(pc);
+            peer_arena = pa;
+            peer_prog = static_cast<int*>(pp);
+        }
+        // every rank's progress reset is done before any kernel reads a peer's
+        AMTC_NCCL(ncclAllReduce(small + SM_WORK2, small + SM_WORK2, 1, ncclInt32, ncclSum, comm, s));
+    }
+    // this rank's strip items, right to left
+    tc_launch_split_expand(static_cast<int*>(st->items[0].p), small + SM_HIST + TC_CLASSES, S, nsp,
+                           static_cast<int*>(st->sp_items.p), small + SM_SPLITN, s, s_lo, s_hi);
+    const size_t wsb = strip_ws_bytes_per_warp(N, 0);
+    const int wpc = strip_warps_per_cta();
+    const int64_t ctas = std::min<int64_t>((int64_t)st->sm_count * st->occupancy,
+                                           (2 * (int64_t)(s_hi - s_lo) + wpc - 1) / wpc);
+    int ovf = 0;
+    if (ctas >= 1 && s_hi > s_lo) {
+        AMTC_CUDA(st->ws.ensure(wsb * wpc * (size_t)ctas));
+        AMTC_CUDA(cudaMemsetAsync(small + SM_WORK, 0, sizeof(int), s));
+        AMTC_CUDA(cudaMemsetAsync(small + SM_OVF0, 0, sizeof(int), s));
+        StripLaunchArgs A;
+        A.in = in;
+        A.N = N;
+        A.out = dq;
+        A.items = static_cast<int*>(st->sp_items.p);
+        A.n_items = small + SM_SPLITN;
+        A.work_counter = small + SM_WORK;
+        A.ovf_items = static_cast<int*>(st->items[1].p);
+        AMTC_CUDA(st->items[1].ensure(sizeof(int) * (size_t)nsp));
+        A.ovf_items = static_cast<int*>(st->items[1].p);
+        A.ovf_count = small + SM_OVF0;
+        A.vertex_sum = reinterpret_cast<unsigned long long*>(small + SM_VSUM);
+        A.ws = static_cast<char*>(st->ws.p);
+        A.ws_stride = wsb;
+        A.level = 0;
+        A.ctas = (int)ctas;
+        A.split_S = S;
+        A.progress = static_cast<int*>(st->sp_progress.p);
+        A.carry = static_cast<char*>(st->sp_carry.p);
+        A.carry_stride = carry_b;
+        A.carena_split = st->sp_arena.p;
+        A.carena_cnt = static_cast<int*>(st->sp_cnt.p);
+        A.carena_split_cap = acap;
+        A.peer_strip = (rank + 1 < nranks) ? s_hi : -1;
+        A.sys_fence = nranks > 1 ? 1 : 0;
+        A.peer_carry = peer_carry;
+        A.peer_carena = peer_arena;
+        A.peer_progress = peer_prog;
+        if (strip_launch(A, s) != STATUS_OK) return cuda_fail(cudaGetLastError(), "strip_kernel launch");
+        AMTC_CUDA(cudaMemcpyAsync(&ovf, small + SM_OVF0, sizeof(int), cudaMemcpyDeviceToHost, s));
+    }
+    // rank 0 holds the quote (root strip); share it -- also the barrier before any
+    // rank reuses buffers a peer may still read
+    if (ovf > 0) tc_launch_mark_capacity(static_cast<int*>(st->items[1].p), 1, dq, s);
+    if (nranks > 1) AMTC_NCCL(ncclBroadcast(dq, dq, sizeof(Quote), ncclUint8, 0, comm, s));
+    launch_status_reduce(dq, 1, small + SM_WORST, s);
+    AMTC_CUDA(cudaMemcpyAsync(out, dq, sizeof(amtc_quote), cudaMemcpyDeviceToHost, s));
+    AMTC_CUDA(cudaStreamSynchronize(s));
+    if (ovf > 0 && out->status == 0) out->status = STATUS_ECAPACITY;
+    if (peer_carry) {
+        cudaIpcCloseMemHandle(peer_carry);
+        cudaIpcCloseMemHandle(peer_arena);
+        cudaIpcCloseMemHandle(peer_prog);
+    }
+    AMTC_CUDA(cudaGetLastError());
+    return out->status;
+}
+
 // host-pointer variants: stage through device buffers
 static size_t soa_bytes(int64_t n) { return (size_t)n * (7 * sizeof(double) + sizeof(int32_t)); }
 
@@ -505,6 +690,14 @@ const char* amtc_strerror(int status) {
 }
 
 const char* amtc_last_error(void) { return g_last_error.c_str(); }
+
+int amtc_tree_shard_plan(int32_t N, int nranks, int32_t* lo) {
+    if (N < 1 || nranks < 1 || !lo) return STATUS_EINVAL;
+    std::vector<int> v;
+    shard_strips(N, nranks, v);
+    for (int g = 0; g <= nranks; ++g) lo[g] = v[g];
+    return STATUS_OK;
+}
 
 void amtc_debug_set_heavy_threshold(int tl) { strip_set_heavy_threshold(tl); }
 

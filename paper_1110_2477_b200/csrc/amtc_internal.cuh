@@ -73,7 +73,17 @@ struct StripLaunchArgs {
     // light kernel (no tier 3) and the first item of the launch (device pointer)
     bool light = false;
     const int* item_lo = nullptr;
+    // sharded single tree (split mode over GPUs)
+    int peer_strip = -1;
+    int sys_fence = 0;
+    char* peer_carry = nullptr;
+    void* peer_carena = nullptr;
+    int* peer_progress = nullptr;
 };
+// the transaction-cost tree sharded over the ranks of an NCCL communicator
+// (amtc_capi.cu); comm is an ncclComm_t
+int tc_tree_sharded(const void* params, int N, const void* payoff, double k, void* comm, int rank, int nranks,
+                    void* out, cudaStream_t s);
 size_t strip_ws_bytes_per_warp_light(int N);
 int strip_light_warps_per_cta();
 int strip_light_ctas_per_sm();
@@ -81,7 +91,7 @@ size_t strip_carry_bytes(int N);
 int strip_split_arena_cap(int N);
 size_t strip_vtx_bytes();
 void tc_launch_split_expand(const int* items, const int* n_items, int S, int64_t max_items, int* out, int* n_out,
-                            cudaStream_t s);
+                            cudaStream_t s, int s_lo = 0, int s_hi = -1);
 size_t strip_ws_bytes_per_warp(int N, int level);
 int strip_warps_per_cta();
 int strip_ctas_per_sm();

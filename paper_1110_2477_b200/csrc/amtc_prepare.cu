@@ -101,18 +101,22 @@ void tc_launch_prepare(const BatchPtrs& in, int64_t n, int N, Quote* out, unsign
 
 // split mode: item c -> S strip items c S + s, strips right to left (s = S-1 .. 0),
 // so a strip is always claimed after the strip whose carry column it reads
-__global__ void tc_split_expand_kernel(const int* items, const int* n_items, int S, int* out, int* n_out) {
+// (a sharded tree keeps only strips [s_lo, s_hi) on this GPU)
+__global__ void tc_split_expand_kernel(const int* items, const int* n_items, int S, int s_lo, int s_hi, int* out,
+                                       int* n_out) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int n = *n_items;
-    if (i == 0) *n_out = n * S;
-    if (i >= (int64_t)n * S) return;
-    const int k = (int)(i / S), q = (int)(i % S);
-    out[i] = items[k] * S + (S - 1 - q);
+    const int n = *n_items, w = s_hi - s_lo;
+    if (i == 0) *n_out = n * w;
+    if (i >= (int64_t)n * w) return;
+    const int k = (int)(i / w), q = (int)(i % w);
+    out[i] = items[k] * S + (s_hi - 1 - q);
 }
 
 void tc_launch_split_expand(const int* items, const int* n_items, int S, int64_t max_items, int* out, int* n_out,
-                            cudaStream_t s) {
-    tc_split_expand_kernel<<<(unsigned)((max_items + 255) / 256), 256, 0, s>>>(items, n_items, S, out, n_out);
+                            cudaStream_t s, int s_lo, int s_hi) {
+    if (s_hi < 0) s_hi = S;
+    tc_split_expand_kernel<<<(unsigned)((max_items + 255) / 256), 256, 0, s>>>(items, n_items, S, s_lo, s_hi, out,
+                                                                                n_out);
     note_launch();
 }
 

@@ -152,6 +152,13 @@ struct StripLaunch {
     int* carena_cnt;        // per tree: its bump counter
     int carena_split_cap;
     const int* item_lo;     // device: first item index of this launch (nullptr: 0)
+    // sharded single tree: strip peer_strip (and its carry arena / progress) is
+    // owned by the next GPU, mapped here through CUDA IPC; -1: none
+    int peer_strip;
+    int sys_fence;          // publish progress with system-scope fences
+    char* peer_carry;
+    Vtx* peer_carena;
+    int* peer_progress;
 };
 
 #define WS(T, field, q) reinterpret_cast<T*>(wb + L.lay.field + (size_t)(q) * L.lay.field##_ps)
@@ -329,8 +336,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
             volatile int* prog_in = nullptr;
             volatile int* prog_out = nullptr;
             if (split) {
-                char* co = L.carry + ((size_t)tree * L.split_S + s) * L.carry_stride;
-                char* ci = co + L.carry_stride;  // strip s+1 (read only when it exists)
+                // strip s+1 may live on the next GPU (sharded tree): its carry
+                // column, carry arena and progress counter are then read through
+                // the peer's memory (CUDA IPC over NVLink)
+                const bool remote = s + 1 == L.peer_strip;
+                const size_t si = (size_t)tree * L.split_S + s;
+                char* co = L.carry + si * L.carry_stride;
+                char* ci = (remote ? L.peer_carry : L.carry) + (si + 1) * L.carry_stride;
                 chdr_o = reinterpret_cast<int2*>(co);
                 csl_o = reinterpret_cast<double*>(co + L.c_csl);
                 cv_o = reinterpret_cast<Vtx*>(co + L.c_cv);
@@ -338,11 +350,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
                 csl_i = reinterpret_cast<const double*>(ci + L.c_csl);
                 cv_i = reinterpret_cast<const Vtx*>(ci + L.c_cv);
                 ca_o = L.carena_split + (size_t)tree * L.carena_split_cap;
-                ca_i = ca_o;
+                ca_i = (remote ? L.peer_carena : L.carena_split) + (size_t)tree * L.carena_split_cap;
                 ccnt = &L.carena_cnt[tree];
                 ccap = L.carena_split_cap;
-                prog_out = L.progress + (size_t)tree * L.split_S + s;
-                prog_in = prog_out + 1;
+                prog_out = L.progress + si;
+                prog_in = (remote ? L.peer_progress : L.progress) + si + 1;
             } else {
                 chdr_o = WS(int2, chdr, cout);
                 csl_o = WS(double, csl, cout);
@@ -553,7 +565,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
                         }
                     }
                     if (prog_out) {  // split mode: publish level t to strip s-1
-                        __threadfence();
+                        if (L.sys_fence) __threadfence_system();  // the reader may be another GPU
+                        else __threadfence();
                         __syncwarp();
                         if (lane == 0) *prog_out = t;
                     }
@@ -565,7 +578,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
                 __syncwarp();
             }
             __syncwarp();
-            if (prog_out && err && lane == 0) *prog_out = -1;  // never leave strip s-1 waiting
+            if (prog_out && err && lane == 0) {  // never leave strip s-1 waiting
+                if (L.sys_fence) __threadfence_system();
+                *prog_out = -1;
+            }
             if (s == 0 && !err) {
                 const Fn mine = (my_off < 0) ? make_fn(&S.row[lane], my_n, my_sl, SW)
                                              : make_fn(WS(Vtx, rarena, cur) + my_off, my_n, my_sl, 1);
@@ -738,6 +754,11 @@ int strip_launch(const StripLaunchArgs& a, cudaStream_t s) {
     L.carena_cnt = a.carena_cnt;
     L.carena_split_cap = a.carena_split_cap;
     L.item_lo = a.item_lo;
+    L.peer_strip = a.peer_strip;
+    L.sys_fence = a.sys_fence;
+    L.peer_carry = a.peer_carry;
+    L.peer_carena = reinterpret_cast<Vtx*>(a.peer_carena);
+    L.peer_progress = a.peer_progress;
     L.caps = a.light ? strip_caps_light(a.N) : strip_caps(a.N, a.level);
     L.lay = strip_layout(a.N, L.caps);
     if (L.lay.total != a.ws_stride) return STATUS_EINVAL;

@@ -345,10 +345,21 @@ int amtc_price_tree_sharded(const amtc_params* params, int32_t N, const amtc_pay
         if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !nccl_comm)) return STATUS_EINVAL;
         if (!(k >= 0.0 && k < 1.0)) return STATUS_EINVAL;
         if (k > 0.0) {
-            // the transaction-cost tree is not sharded yet: one GPU only
-            if (nranks != 1) return STATUS_EINVAL;
-            *out = amtc_price_american_tc(params, N, payoff, k);
-            return out->status;
+            // the transaction-cost tree: strips partitioned over the ranks, the
+            // boundary carry column read from the next GPU (amtc_capi.cu)
+            if (nranks == 1 && !nccl_comm) {
+                *out = amtc_price_american_tc(params, N, payoff, k);
+                return out->status;
+            }
+            if (!params || !payoff || payoff->flags != 0) return STATUS_EINVAL;
+            if (N < 64) {  // too small to shard: every rank prices it alone
+                *out = amtc_price_american_tc(params, N, payoff, k);
+                return out->status;
+            }
+            const int st = tc_tree_sharded(params, N, payoff, k, nccl_comm, rank, nranks, out,
+                                           static_cast<cudaStream_t>(cuda_stream));
+            out->status = st;
+            return st;
         }
         TreeConsts c;
         int st = tree_consts(params, N, payoff, c);

@@ -81,14 +81,16 @@ def test_sharded_one_rank_nccl(api):
             q = api.price_tree_sharded(100.0, 100.0, 1.0, 0.3, 0.05, N, 0.0, O.PUT, comm=comm, rank=0, nranks=1)
             o = O.price_crr(O.Option(100.0, 100.0, 1.0, 0.3, 0.05, 0.0, O.PUT), N)
             assert q["status"] == 0 and _close(q["ask"], o) and q["bid"] == q["ask"], (q, o)
-        q = api.price_tree_sharded(100.0, 100.0, 1.0, 0.3, 0.05, 200, 0.005, O.PUT, comm=comm, rank=0, nranks=1)
-        o = O.price_tc(O.Option(100.0, 100.0, 1.0, 0.3, 0.05, 0.005, O.PUT), 200)
-        assert q["status"] == 0 and _close(q["ask"], o.ask) and _close(q["bid"], o.bid), (q, o)
+        # k > 0 through the sharded transaction-cost path (one rank: no peer)
+        for N, kind, K, k in ((200, O.PUT, 100.0, 0.005), (300, O.CALL, 95.0, 0.02), (1000, O.PUT, 100.0, 0.005)):
+            q = api.price_tree_sharded(100.0, K, 1.0, 0.3, 0.05, N, k, kind, comm=comm, rank=0, nranks=1)
+            o = O.price_tc(O.Option(100.0, K, 1.0, 0.3, 0.05, k, kind), N)
+            assert q["status"] == 0 and _close(q["ask"], o.ask) and _close(q["bid"], o.bid), (N, q, o)
     finally:
         api.comm_destroy(comm)
     # no communicator, one rank
     q = api.price_tree_sharded(100.0, 100.0, 1.0, 0.3, 0.05, 300, 0.0, O.PUT)
     assert q["status"] == 0
-    # k > 0 cannot be sharded yet
+    # several ranks need a communicator
     q = api.price_tree_sharded(100.0, 100.0, 1.0, 0.3, 0.05, 300, 0.005, O.PUT, comm=None, rank=0, nranks=2)
     assert q["status"] == 1 and math.isnan(q["ask"])
