@@ -418,6 +418,27 @@ def run_tree(args):
     clocks = sampler.stop() if sampler else None
     tot = max_over_ranks(float(np.sum(times)), pg, dev)
     value = nodes * args.steps / tot
+    extra = None
+    if args.config == 5:
+        # config 5b: the transaction-cost tree, sharded the same way (k > 0 path)
+        r5 = W.config5b().row(0)
+        def step5b():
+            q = api.price_tree_sharded(r5["S0"], r5["K"], r5["T"], r5["sigma"], r5["R"], W.CONFIG5B_N, r5["k"],
+                                       api.PUT, comm=comm, rank=rank, nranks=world)
+            assert q["status"] == 0, q
+            return q
+        step5b()
+        torch.cuda.synchronize()
+        t5 = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            q5 = step5b()
+            torch.cuda.synchronize()
+            t5.append(time.perf_counter() - t0)
+        tot5 = max_over_ranks(float(np.sum(t5)), pg, dev)
+        extra = {"config5b": {"N": W.CONFIG5B_N, "k": r5["k"], "ms_per_step": 1e3 * tot5 / args.steps,
+                              "node_updates_per_s": tc_nodes(W.CONFIG5B_N) * args.steps / tot5,
+                              "ask": q5["ask"], "bid": q5["bid"]}}
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         opt, Ns, kind = cpu_sample
@@ -440,6 +461,8 @@ def run_tree(args):
                            "l2": "inputs are scalars; levels live in HBM/L2 between bands"},
                 "roofline": None, "cpu_baseline": cpu, "e2e": None, "clocks": clocks,
                 "step_ms": [1e3 * t for t in times]}
+        if extra:
+            line["extra"] = extra
         print(json.dumps(line), flush=True)
     if comm is not None:
         api.comm_destroy(comm)
