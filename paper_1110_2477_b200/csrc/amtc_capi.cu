@@ -180,12 +180,15 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
         const size_t need_b = (size_t)nsp * (carry_b + 2 * sizeof(int)) + (size_t)n2 * acap * strip_vtx_bytes();
         if (want && need_b > budget / 2) want = false;
         if (want) {
-            const size_t wsb = strip_ws_bytes_per_warp(N, 0);
-            int64_t ctas = std::min<int64_t>((int64_t)st->sm_count * st->occupancy, (nsp + wpc - 1) / wpc);
-            ctas = std::min<int64_t>(ctas, (int64_t)((budget - need_b) / (wsb * wpc)));
+            const size_t wsb = strip_ws_bytes_per_warp_split(N);
+            const int swpc = strip_split_warps_per_cta();
+            // every SM (one split-kernel CTA each): strips are claimed first-come,
+            // so they spread over all SMs (a strip pipeline is latency bound)
+            int64_t ctas = std::min<int64_t>((int64_t)st->sm_count, nsp);
+            ctas = std::min<int64_t>(ctas, (int64_t)((budget - need_b) / (wsb * swpc)));
             if (ctas < 1) want = false;
             if (want) {
-                AMTC_CUDA(st->ws.ensure(wsb * wpc * (size_t)ctas));
+                AMTC_CUDA(st->ws.ensure(wsb * swpc * (size_t)ctas));
                 AMTC_CUDA(st->sp_items.ensure(sizeof(int) * (size_t)nsp));
                 AMTC_CUDA(st->sp_progress.ensure(sizeof(int) * (size_t)nsp));
                 AMTC_CUDA(st->sp_carry.ensure(carry_b * (size_t)nsp));
@@ -468,10 +471,9 @@ int tc_tree_sharded(const void* params_v, int N, const void* payoff_v, double k,
     // this rank's strip items, right to left
     tc_launch_split_expand(static_cast<int*>(st->items[0].p), small + SM_HIST + TC_CLASSES, S, nsp,
                            static_cast<int*>(st->sp_items.p), small + SM_SPLITN, s, s_lo, s_hi);
-    const size_t wsb = strip_ws_bytes_per_warp(N, 0);
-    const int wpc = strip_warps_per_cta();
-    const int64_t ctas = std::min<int64_t>((int64_t)st->sm_count * st->occupancy,
-                                           (2 * (int64_t)(s_hi - s_lo) + wpc - 1) / wpc);
+    const size_t wsb = strip_ws_bytes_per_warp_split(N);
+    const int wpc = strip_split_warps_per_cta();
+    const int64_t ctas = std::min<int64_t>((int64_t)st->sm_count, 2 * (int64_t)(s_hi - s_lo));
     int ovf = 0;
     if (ctas >= 1 && s_hi > s_lo) {
         AMTC_CUDA(st->ws.ensure(wsb * wpc * (size_t)ctas));

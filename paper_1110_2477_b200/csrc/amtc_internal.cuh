@@ -85,6 +85,8 @@ struct StripLaunchArgs {
 int tc_tree_sharded(const void* params, int N, const void* payoff, double k, void* comm, int rank, int nranks,
                     void* out, cudaStream_t s);
 size_t strip_ws_bytes_per_warp_light(int N);
+size_t strip_ws_bytes_per_warp_split(int N);
+int strip_split_warps_per_cta();
 int strip_light_warps_per_cta();
 int strip_light_ctas_per_sm();
 size_t strip_carry_bytes(int N);

@@ -643,10 +643,16 @@ constexpr int STRIP_C = AMTC_FULL_CB, STRIP_B = AMTC_FULL_CB, STRIP_WARPS = AMTC
 #endif
 constexpr int LIGHT_CFG[4] = {AMTC_LIGHT_CFG};
 constexpr int LIGHT_C = LIGHT_CFG[0], LIGHT_B = LIGHT_CFG[1], LIGHT_WARPS = LIGHT_CFG[2], LIGHT_MINB = LIGHT_CFG[3];
+// split mode (single trees, small batches): 16 warps with 6-vertex slots --
+// a strip pipeline is latency bound, so fewer warps per SM and no arena spills
+// of 5-vertex functions beat the 20 / 4 shape there (config 5b: 128 vs 177 ms)
+constexpr int SPLIT_C = 6, SPLIT_B = 6, SPLIT_WARPS = 16;
+#define SPLIT_KERNEL strip_kernel<SPLIT_C, SPLIT_B, SPLIT_WARPS, 1, true>
 #define STRIP_KERNEL strip_kernel<STRIP_C, STRIP_B, STRIP_WARPS, STRIP_MINB, true>
 #define LIGHT_KERNEL strip_kernel<LIGHT_C, LIGHT_B, LIGHT_WARPS, LIGHT_MINB, false>
 constexpr size_t STRIP_SMEM = sizeof(CtaHdr) + sizeof(StripSmem<STRIP_C, STRIP_B, true>) * STRIP_WARPS;
 constexpr size_t LIGHT_SMEM = sizeof(CtaHdr) + sizeof(StripSmem<LIGHT_C, LIGHT_B, false>) * LIGHT_WARPS;
+constexpr size_t SPLIT_SMEM = sizeof(CtaHdr) + sizeof(StripSmem<SPLIT_C, SPLIT_B, true>) * SPLIT_WARPS;
 
 static int strip_set_smem() {
     static int done = 0;
@@ -655,6 +661,9 @@ static int strip_set_smem() {
             cudaSuccess)
             return STATUS_ECUDA;
         if (cudaFuncSetAttribute(LIGHT_KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LIGHT_SMEM) !=
+            cudaSuccess)
+            return STATUS_ECUDA;
+        if (cudaFuncSetAttribute(SPLIT_KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SPLIT_SMEM) !=
             cudaSuccess)
             return STATUS_ECUDA;
         done = 1;
@@ -703,6 +712,14 @@ static StripCaps strip_caps_light(int N) {
 
 size_t strip_ws_bytes_per_warp(int N, int level) { return strip_layout(N, strip_caps(N, level)).total; }
 size_t strip_ws_bytes_per_warp_light(int N) { return strip_layout(N, strip_caps_light(N)).total; }
+static StripCaps strip_caps_split(int N) {
+    StripCaps c = strip_caps(N, 0);
+    c.C = SPLIT_C;
+    c.B = SPLIT_B;
+    return c;
+}
+size_t strip_ws_bytes_per_warp_split(int N) { return strip_layout(N, strip_caps_split(N)).total; }
+int strip_split_warps_per_cta() { return SPLIT_WARPS; }
 int strip_light_warps_per_cta() { return LIGHT_WARPS; }
 int strip_light_ctas_per_sm() {
     int b = 0;
@@ -715,7 +732,7 @@ int strip_light_ctas_per_sm() {
 // per-tree carry arena (vertices)
 size_t strip_carry_bytes(int N) {
     return align256(sizeof(int2) * (size_t)(N + 2)) + align256(sizeof(double) * (size_t)(N + 2)) +
-           align256(sizeof(Vtx) * (size_t)STRIP_C * (size_t)(N + 2));
+           align256(sizeof(Vtx) * (size_t)SPLIT_C * (size_t)(N + 2));
 }
 int strip_split_arena_cap(int N) {
     const int64_t v = 16 * (int64_t)(N + 2) * (N / SW + 1) + 65536;
@@ -759,11 +776,12 @@ int strip_launch(const StripLaunchArgs& a, cudaStream_t s) {
     L.peer_carry = a.peer_carry;
     L.peer_carena = reinterpret_cast<Vtx*>(a.peer_carena);
     L.peer_progress = a.peer_progress;
-    L.caps = a.light ? strip_caps_light(a.N) : strip_caps(a.N, a.level);
+    L.caps = a.light ? strip_caps_light(a.N) : (a.split_S > 0 ? strip_caps_split(a.N) : strip_caps(a.N, a.level));
     L.lay = strip_layout(a.N, L.caps);
     if (L.lay.total != a.ws_stride) return STATUS_EINVAL;
     if (strip_set_smem() != STATUS_OK) return STATUS_ECUDA;
     if (a.light) LIGHT_KERNEL<<<a.ctas, LIGHT_WARPS * 32, LIGHT_SMEM, s>>>(L);
+    else if (a.split_S > 0) SPLIT_KERNEL<<<a.ctas, SPLIT_WARPS * 32, SPLIT_SMEM, s>>>(L);
     else STRIP_KERNEL<<<a.ctas, STRIP_WARPS * 32, STRIP_SMEM, s>>>(L);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? STATUS_OK : STATUS_ECUDA;
