@@ -45,8 +45,13 @@ __device__ __forceinline__ double crr_tree(int lane, int N, double S0, double K,
     const double p = (r - d) / (u - d);
     const double pu = p / r, pd = (1.0 - p) / r;
     const double c0 = (KIND == KIND_PUT) ? K * (1.0 - d) : -K * (1.0 - d);
+    // along a lane's block, S_{t,j+1} = d^2 S_{t,j}: X_{q+1} = d^2 X_q + c2
+    const double d2 = d * d;
+    const double c2 = (KIND == KIND_PUT) ? K * (1.0 - d2) : -K * (1.0 - d2);
 
-    double V[C][CRR_M], X[C][CRR_M];
+    // only the first node's exercise state of each slot is carried (registers:
+    // C instead of C x M), the others are rebuilt along the block every level
+    double V[C][CRR_M], Xb[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
 #pragma unroll
@@ -57,7 +62,7 @@ __device__ __forceinline__ double crr_tree(int lane, int N, double S0, double K,
             if (KIND == KIND_PUT) x = K - S;
             else if (KIND == KIND_CALL) x = S - K;
             else x = S;  // bull: X holds S
-            X[c][q] = x;
+            if (q == 0) Xb[c] = x;
             V[c][q] = (KIND == KIND_BULL) ? fmin(fmax(S - K, 0.0), K2 - K) : fmax(x, 0.0);
         }
     }
@@ -67,16 +72,19 @@ __device__ __forceinline__ double crr_tree(int lane, int N, double S0, double K,
             if (32 * c * CRR_M > t) break;  // warp-uniform: slot c holds no live node
             const double send = (lane == 0) ? ((c + 1 < C) ? V[c + 1][0] : 0.0) : V[c][0];
             const double nb = __shfl_sync(0xffffffffu, send, (lane + 1) & 31);
+            double x;
+            if (KIND == KIND_BULL) x = (Xb[c] *= d);
+            else x = Xb[c] = fma(d, Xb[c], c0);
 #pragma unroll
             for (int q = 0; q < CRR_M; ++q) {
                 const double vn = (q + 1 < CRR_M) ? V[c][q + 1] : nb;
                 double ex;
                 if (KIND == KIND_BULL) {
-                    X[c][q] *= d;
-                    ex = min_nonneg(max_nonneg(X[c][q] - K, 0.0), K2 - K);
+                    ex = min_nonneg(max_nonneg(x - K, 0.0), K2 - K);
+                    x *= d2;
                 } else {
-                    X[c][q] = fma(d, X[c][q], c0);
-                    ex = X[c][q];
+                    ex = x;
+                    x = fma(d2, x, c2);
                 }
                 V[c][q] = max_nonneg(ex, fma(pu, V[c][q], pd * vn));
             }
@@ -85,8 +93,11 @@ __device__ __forceinline__ double crr_tree(int lane, int N, double S0, double K,
     return V[0][0];
 }
 
+#ifndef AMTC_CRR_MINB
+#define AMTC_CRR_MINB 1
+#endif
 template <int C>
-__global__ void __launch_bounds__(CRR_THREADS) crr_kernel(BatchPtrs in, int64_t n, int N, double* out) {
+__global__ void __launch_bounds__(CRR_THREADS, AMTC_CRR_MINB) crr_kernel(BatchPtrs in, int64_t n, int N, double* out) {
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= n) return;
