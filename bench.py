@@ -189,7 +189,12 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": float(np.mean([args.ref_options * tc_nodes(N) / r["value"] * 1e3 for r in times])),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": desc, "N": N, "options_per_step": args.ref_options},
+            "data": "synthetic",
+            "config": {"workload": desc, "N": N, "options_per_gpu": len(b), "options_total": len(b),
+                       "node_updates_per_option": tc_nodes(N) if args.config == 4 else crr_nodes(N),
+                       "parallelism": "host cores, one option per thread",
+                       "reference_sample": f"each step prices a seeded sample of {args.ref_options} options of "
+                                           "this workload (bounded CPU time)"},
             "cpu_baseline": {"value": value, "unit": "node-updates/s", "cores": times[-1]["cores"],
                              "kind": "oracle", "sample": times[-1]["sample"]},
             "e2e": {"value": value, "unit": "node-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
