@@ -130,6 +130,19 @@ CONFIG5A_N = 100000
 CONFIG5B_N = 8000
 
 
+def fig9(N_levels: int = 1000) -> Batch:
+    """the paper's Fig. 9 price curves -- the
+    Example 5.1 put (K=100, T=0.25, sigma=0.2, R=0.1) for S0 in {90, 91, ..., 110}
+    and k in {0, 0.25%, 0.5%}, as one batch (k-major), to be priced at N=1000
+    (reading A16)."""
+    S0 = np.repeat(np.arange(90.0, 111.0)[None, :], 3, axis=0).ravel()
+    k = np.repeat(np.array([0.0, 0.0025, 0.005]), 21)
+    return _batch(S0, np.full(S0.shape, 100.0), 0.0, 0.25, 0.2, 0.1, k, PUT)
+
+
+FIG9_N = 1000
+
+
 def appendix_put() -> Batch:
     """Appendix workload: put K=S0=100, T=3, sigma=0.3, R=0.06."""
     return _batch(100.0, [100.0], 0.0, 3.0, 0.3, 0.06, 0.0, PUT)

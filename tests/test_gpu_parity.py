@@ -298,3 +298,19 @@ def test_capacity_retry_passes(api):
     np.testing.assert_allclose(got["bid"], ref["bid"], rtol=1e-12, atol=1e-12)
     assert rc2 == 3 and np.any(bad["status"] == 3)  # AMTC_ECAPACITY
     assert np.all(np.isnan(bad["ask"][bad["status"] == 3]))
+
+
+def test_fig9_curves(api):
+    """the Fig. 9 workload as one batch at
+    N=1000 -- parity with the oracle for all 63 points and the paper's ordering
+    chain pi^b_k2 <= pi^b_k1 <= pi_k0 < pi^a_k1 < pi^a_k2 at every S0."""
+    b = W.fig9()
+    N = W.FIG9_N
+    got, rc = api.price_american_tc_batch_host(b, N)
+    assert rc == 0
+    want = O.price_tc_many([_opt(b.row(i)) for i in range(len(b))], N)
+    assert_quotes(got, b, N, want)
+    a, bid = got["ask"].reshape(3, 21), got["bid"].reshape(3, 21)
+    np.testing.assert_allclose(a[0], bid[0], rtol=1e-9)        # k = 0: ask = bid = CRR
+    assert np.all(bid[2] <= bid[1] + 1e-10) and np.all(bid[1] <= bid[0] + 1e-10)
+    assert np.all(a[0] < a[1]) and np.all(a[1] < a[2])
