@@ -91,6 +91,17 @@ amtc_quote amtc_price_american_tc(const amtc_params* params, int32_t N, const am
                                   double k);
 
 /*
+ * As amtc_price_american_tc, plus the root hedge: the
+ * share position the seller (*y_ask) and the buyer (*y_bid) take at t = 0,
+ * argmin_y [ w_0(y)/r + S0 y ] over the vertices of w_0 = max(z_{1,0}, z_{1,1})
+ * (no costs at t = 0; derived A.4; smallest minimiser on ties).  At k = 0
+ * it is the CRR delta (pi^u - pi^d)/(S0 (u - d)) and its negative (derived A.1).
+ * out, y_ask, y_bid: HOST pointers; NaN on error.  Synchronous.  Returns the status.
+ */
+int amtc_price_american_tc_hedge(const amtc_params* params, int32_t N, const amtc_payoff* payoff, double k,
+                                 amtc_quote* out, double* y_ask, double* y_bid);
+
+/*
  * Batched ask/bid for n independent options on N-step trees (DEVICE pointers).
  * d_out: device array of n amtc_quote.  Work is enqueued on cuda_stream
  * (a cudaStream_t, NULL = legacy default stream); the call synchronises that

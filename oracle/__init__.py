@@ -55,7 +55,7 @@ class _Quote(C.Structure):
     _fields_ = [("ask", C.c_double), ("bid", C.c_double), ("status", C.c_int32),
                 ("max_kinks_ask", C.c_int32), ("max_kinks_bid", C.c_int32), ("pad", C.c_int32),
                 ("sum_kinks_ask", C.c_int64), ("sum_kinks_bid", C.c_int64),
-                ("crossings", C.c_int64)]
+                ("crossings", C.c_int64), ("hedge_ask", C.c_double), ("hedge_bid", C.c_double)]
 
 
 _lib = None
@@ -108,6 +108,8 @@ class Quote:
     sum_kinks_ask: int
     sum_kinks_bid: int
     crossings: int
+    hedge_ask: float = float("nan")
+    hedge_bid: float = float("nan")
 
 
 def price_tc(opt: Option, N: int, kinks: bool = False):
@@ -122,7 +124,7 @@ def price_tc(opt: Option, N: int, kinks: bool = False):
     o = opt._c()
     lib().oracle_price_tc(C.byref(o), N, C.byref(q), ptr)
     out = Quote(q.ask, q.bid, q.status, q.max_kinks_ask, q.max_kinks_bid, q.sum_kinks_ask,
-                q.sum_kinks_bid, q.crossings)
+                q.sum_kinks_bid, q.crossings, q.hedge_ask, q.hedge_bid)
     return (out, arr) if kinks else out
 
 

@@ -433,6 +433,11 @@ typedef struct {
     int32_t pad;
     int64_t sum_kinks_ask, sum_kinks_bid; /* over all nodes t <= N */
     int64_t crossings;
+    /* root hedge: the share position y* the seller /
+       buyer takes at t = 0, argmin_y [ w_0(y)/r + S0 y ] over the vertices of
+       w_0 = max(z_{1,0}, z_{1,1}) (no costs at t = 0, so v_0 is the line
+       min_y'[w_0(y')/r + S0 y'] - S0 y, derived A.4); smallest minimiser */
+    double hedge_ask, hedge_bid;
 } or_quote;
 
 /* Sec. 4.1: u = exp(sigma sqrt(T/N)), d = 1/u, r = exp(RT/N) */
@@ -522,6 +527,19 @@ int oracle_price_tc(const or_option *o, int N, or_quote *q, int32_t *kinks_out)
             double xi, zeta;
             payoff(o, S, &xi, &zeta);
             for (int party = 0; party < 2 && st == OR_OK; party++) {
+                if (t == 0) {
+                    /* root hedge: argmin over the vertices of w_0 of w_0(x)/r + S0 x (A.4) */
+                    pwl w;
+                    if ((st = pwl_envelope(&z[party][0], &z[party][1], 1, &w, &cnt)) != OR_OK) break;
+                    double best = INFINITY, bx = NAN;
+                    for (int i = 0; i < w.n; i++) {
+                        double g = w.f[i] / r + S * w.x[i];
+                        if (g < best) { best = g; bx = w.x[i]; }
+                    }
+                    pwl_free(&w);
+                    if (party == 0) q->hedge_ask = bx;
+                    else q->hedge_bid = bx;
+                }
                 pwl znew;
                 st = node_update(party, &z[party][j], &z[party][j + 1], r, Sa, Sb, xi, zeta, &znew, &cnt);
                 if (st != OR_OK) break;

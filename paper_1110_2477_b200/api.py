@@ -51,7 +51,7 @@ EXPORTS = ["amtc_price_american_tc", "amtc_price_american_tc_batch", "amtc_price
            "amtc_launch_count", "amtc_tc_last_stats", "amtc_debug_set_heavy_threshold",
            "amtc_price_crr_tree", "amtc_comm_unique_id", "amtc_comm_init", "amtc_comm_destroy",
            "amtc_price_tree_sharded", "amtc_debug_set_split_mode", "amtc_debug_set_light_kernel",
-           "amtc_debug_set_arena_shift", "amtc_tree_shard_plan"]
+           "amtc_debug_set_arena_shift", "amtc_tree_shard_plan", "amtc_price_american_tc_hedge"]
 
 _lib = None
 
@@ -87,6 +87,8 @@ def lib():
         L.amtc_price_tree_sharded.argtypes = [C.POINTER(Params), C.c_int32, C.POINTER(Payoff), C.c_double,
                                               C.c_void_p, C.c_int, C.c_int, C.POINTER(Quote), C.c_void_p]
         L.amtc_tree_shard_plan.argtypes = [C.c_int32, C.c_int, C.POINTER(C.c_int32)]
+        L.amtc_price_american_tc_hedge.argtypes = [C.POINTER(Params), C.c_int32, C.POINTER(Payoff), C.c_double,
+                                                   C.POINTER(Quote), C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.amtc_debug_set_arena_shift.restype = None
         L.amtc_debug_set_arena_shift.argtypes = [C.c_int]
         L.amtc_debug_set_light_kernel.restype = None
@@ -312,3 +314,15 @@ def tree_shard_plan(N: int, nranks: int) -> list:
     if rc:
         raise ValueError(f"amtc_tree_shard_plan: {STATUS.get(rc, rc)}")
     return list(lo)
+
+
+def price_american_tc_hedge(S0: float, K: float, T: float, sigma: float, R: float, N: int, k: float,
+                            kind: int = PUT, K2: float = 0.0) -> dict:
+    """Ask, bid and the root hedges (positions at t = 0) of one option."""
+    p = Params(S0, T, sigma, R)
+    y = Payoff(kind, 0, K, K2)
+    q = Quote()
+    ya, yb = C.c_double(), C.c_double()
+    lib().amtc_price_american_tc_hedge(C.byref(p), N, C.byref(y), k, C.byref(q), C.byref(ya), C.byref(yb))
+    return {"ask": q.ask, "bid": q.bid, "status": q.status, "max_bp": q.max_bp, "hedge_ask": ya.value,
+            "hedge_bid": yb.value}

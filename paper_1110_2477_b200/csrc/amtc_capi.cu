@@ -114,7 +114,7 @@ static int g_light_kernel = 1;
 constexpr int kMaxLevel = 4;
 
 static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amtc_quote* d_out,
-                           cudaStream_t s) {
+                           cudaStream_t s, double* d_hedge = nullptr) {
     if (!soa_ok(d_in) || !d_out || n < 0 || N < 1) return STATUS_EINVAL;
     if (n == 0) return STATUS_OK;
     if (2 * n > (int64_t)INT32_MAX / 2) return STATUS_EINVAL;
@@ -222,6 +222,7 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
                 A.carena_split = st->sp_arena.p;
                 A.carena_cnt = static_cast<int*>(st->sp_cnt.p);
                 A.carena_split_cap = acap;
+                A.hedge = d_hedge;
                 if (strip_launch(A, s) != STATUS_OK) return cuda_fail(cudaGetLastError(), "strip_kernel launch");
                 AMTC_CUDA(cudaEventRecord(st->ev[1], s));
                 passes = 1;
@@ -290,6 +291,7 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
                 AL.level = 0;
                 AL.ctas = (int)lctas;
                 AL.light = true;
+                AL.hedge = d_hedge;
             }
         }
         StripLaunchArgs A;
@@ -306,6 +308,7 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
         A.ws_stride = wsb;
         A.level = level;
         A.ctas = (int)ctas;
+        A.hedge = d_hedge;
         if (light_pass) AMTC_CUDA(cudaEventRecord(st->ev_fork, s));
         if (strip_launch(A, s) != STATUS_OK) return cuda_fail(cudaGetLastError(), "strip_kernel launch");
         if (light_pass) {
@@ -633,6 +636,49 @@ amtc_quote amtc_price_american_tc(const amtc_params* params, int32_t N, const am
     int rc = amtc_price_american_tc_batch_host(&h, 1, N, &q, nullptr);
     if (rc == STATUS_ECUDA || (rc == STATUS_EINVAL && N < 1)) q.status = rc;
     return q;
+}
+
+int amtc_price_american_tc_hedge(const amtc_params* params, int32_t N, const amtc_payoff* payoff, double k,
+                                 amtc_quote* out, double* y_ask, double* y_bid) {
+    try {
+        if (!out || !y_ask || !y_bid) return STATUS_EINVAL;
+        out->ask = out->bid = NAN;
+        out->max_bp = 0;
+        out->status = STATUS_EINVAL;
+        *y_ask = *y_bid = NAN;
+        if (!params || !payoff || payoff->flags != 0) return STATUS_EINVAL;
+        double S0 = params->S0, K = payoff->K, K2 = payoff->K2, T = params->T, sg = params->sigma, R = params->R;
+        double kk = k;
+        int32_t kind = payoff->kind;
+        amtc_batch_soa h;
+        h.S0 = &S0; h.K = &K; h.K2 = &K2; h.T = &T; h.sigma = &sg; h.R = &R; h.k = &kk; h.kind = &kind;
+        cudaStream_t s = nullptr;
+        int dev = 0;
+        AMTC_CUDA(cudaGetDevice(&dev));
+        DevState* st = state_for_device(dev);
+        amtc_batch_soa d;
+        {
+            std::lock_guard<std::mutex> g(st->mu);
+            int rc = stage_in(st, &h, 1, &d, s);
+            if (rc) return rc;
+            AMTC_CUDA(st->stage_out.ensure(sizeof(amtc_quote) + 4 * sizeof(double)));
+        }
+        amtc_quote* d_out = static_cast<amtc_quote*>(st->stage_out.p);
+        double* d_hedge = reinterpret_cast<double*>(static_cast<char*>(st->stage_out.p) + 32);
+        AMTC_CUDA(cudaMemsetAsync(d_hedge, 0xff, 2 * sizeof(double), s));  // NaN unless written
+        int rc = tc_batch_device(&d, 1, N, d_out, s, d_hedge);
+        if (rc == STATUS_ECUDA) return rc;
+        double hy[2];
+        AMTC_CUDA(cudaMemcpyAsync(out, d_out, sizeof(amtc_quote), cudaMemcpyDeviceToHost, s));
+        AMTC_CUDA(cudaMemcpyAsync(hy, d_hedge, sizeof(hy), cudaMemcpyDeviceToHost, s));
+        AMTC_CUDA(cudaStreamSynchronize(s));
+        *y_ask = out->status ? NAN : hy[0];
+        *y_bid = out->status ? NAN : hy[1];
+        return out->status;
+    } catch (...) {
+        g_last_error = "unexpected host exception";
+        return STATUS_ECUDA;
+    }
 }
 
 int amtc_price_crr_batch(const amtc_batch_soa* d_in, int64_t n, int32_t N, double* d_price, void* cuda_stream) {

@@ -79,6 +79,7 @@ struct StripLaunchArgs {
     char* peer_carry = nullptr;
     void* peer_carena = nullptr;
     int* peer_progress = nullptr;
+    double* hedge = nullptr;  // optional root hedges (2 n doubles, device)
 };
 // the transaction-cost tree sharded over the ranks of an NCCL communicator
 // (amtc_capi.cu); comm is an ncclComm_t

@@ -159,6 +159,7 @@ struct StripLaunch {
     char* peer_carry;
     Vtx* peer_carena;
     int* peer_progress;
+    double* hedge;          // optional: root hedge per (option, party) (2 n doubles)
 };
 
 #define WS(T, field, q) reinterpret_cast<T*>(wb + L.lay.field + (size_t)(q) * L.lay.field##_ps)
@@ -254,10 +255,10 @@ __device__ __noinline__ bool serve_one(CtaHdr& H, StripSmem<C, B, true>* all, in
 
 // a6: root, t = 0, no costs (derived A.4): v_0(y) = min_b [w_0(b) + S0 b] - S0 y
 // over the vertices b of w_0 = max(z_{1,0}, z_{1,1}); returns the status bits.
-__device__ __noinline__ int root_phase(Fn mine, OptionConsts oc, bool seller, Quote* q, int lane) {
+__device__ __noinline__ int root_phase(Fn mine, OptionConsts oc, bool seller, Quote* q, double* hedge, int lane) {
     const Fn Ur = shfl_fn(mine, 0), Dr = shfl_fn(mine, 1);
-    double slW, srW;
-    const double mv = heavy::root_min(Ur, Dr, oc.S0, slW, srW, lane);
+    double slW, srW, ymin;
+    const double mv = heavy::root_min(Ur, Dr, oc.S0, slW, srW, ymin, lane);
     // the minimum exists iff w_0 + S0 y has a decreasing left and increasing right tail
     if (!(slW + oc.S0 < 0.0) || !(srW + oc.S0 > 0.0)) return DEV_UNBOUNDED;
     if (lane == 0) {
@@ -266,6 +267,7 @@ __device__ __noinline__ int root_phase(Fn mine, OptionConsts oc, bool seller, Qu
         const double intrinsic = xi + zeta * oc.S0;  // u_0(0): S^a_0 = S^b_0 = S0
         if (seller) q->ask = fmax(intrinsic, mv);    // pi^a = z_0(0)
         else q->bid = fmax(intrinsic, -mv);          // pi^b = -z'_0(0)
+        if (hedge) *hedge = ymin;                    // the position taken at t = 0 (NEXT #2)
     }
     return DEV_OK;
 }
@@ -585,7 +587,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
             if (s == 0 && !err) {
                 const Fn mine = (my_off < 0) ? make_fn(&S.row[lane], my_n, my_sl, SW)
                                              : make_fn(WS(Vtx, rarena, cur) + my_off, my_n, my_sl, 1);
-                err |= root_phase(mine, oc, seller, &L.out[opt], lane);
+                err |= root_phase(mine, oc, seller, &L.out[opt], L.hedge ? &L.hedge[2 * opt + (seller ? 0 : 1)] : nullptr,
+                                  lane);
             }
         }
         // per-item bookkeeping
@@ -776,6 +779,7 @@ int strip_launch(const StripLaunchArgs& a, cudaStream_t s) {
     L.peer_carry = a.peer_carry;
     L.peer_carena = reinterpret_cast<Vtx*>(a.peer_carena);
     L.peer_progress = a.peer_progress;
+    L.hedge = a.hedge;
     L.caps = a.light ? strip_caps_light(a.N) : (a.split_S > 0 ? strip_caps_split(a.N) : strip_caps(a.N, a.level));
     L.lay = strip_layout(a.N, L.caps);
     if (L.lay.total != a.ws_stride) return STATUS_EINVAL;

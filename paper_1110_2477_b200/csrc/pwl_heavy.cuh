@@ -1204,20 +1204,29 @@ __device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo,
 
 // a6 helper: min over the vertices b of W = max(U, D) of W(b) + S0 b, and W's
 // tail slopes (for the boundedness check)
-__device__ __noinline__ double root_min(const Fn U, const Fn D, double S0, double& slW, double& srW, int lane) {
+// (also the minimiser: the root hedge y*, smallest x on ties)
+__device__ __noinline__ double root_min(const Fn U, const Fn D, double S0, double& slW, double& srW, double& ymin,
+                                        int lane) {
     const HCtx h = make_ctx(U, D);
     const int nb = (h.nE + 31) / 32;
-    double mv = INFINITY;
+    double mv = INFINITY, mx = INFINITY;
     for (int blk = 0; blk < nb; ++blk) {
         const BlockW B = block_w(h, blk, lane);
         for (int q = 0; q < B.w.n; ++q) {
             const WV w = B.w.get(q);
-            mv = fmin(mv, fma(S0, w.x, w.f));
+            const double g = fma(S0, w.x, w.f);
+            if (g < mv || (g == mv && w.x < mx)) { mv = g; mx = w.x; }
         }
     }
     slW = h.tailL_U ? U.sl : D.sl;
     srW = h.wInf_U ? U.v(U.n - 1).s : D.v(D.n - 1).s;
-    return warp_min(mv);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(FULLM, mv, o), ox = __shfl_xor_sync(FULLM, mx, o);
+        if (ov < mv || (ov == mv && ox < mx)) { mv = ov; mx = ox; }
+    }
+    ymin = mx;
+    return mv;
 }
 
 }  // namespace heavy

@@ -314,3 +314,20 @@ def test_fig9_curves(api):
     np.testing.assert_allclose(a[0], bid[0], rtol=1e-9)        # k = 0: ask = bid = CRR
     assert np.all(bid[2] <= bid[1] + 1e-10) and np.all(bid[1] <= bid[0] + 1e-10)
     assert np.all(a[0] < a[1]) and np.all(a[1] < a[2])
+
+
+@pytest.mark.parametrize("N", [5, 60, 400])
+def test_root_hedge(api, N):
+    """the root hedges (positions at t = 0) through
+    amtc_price_american_tc_hedge against the oracle's; at k = 0 they are the
+    CRR delta and its negative (pinned in test_oracle_identities.py)."""
+    b = W.random_small(16, seed=7000 + N, k_max=0.03)
+    b.k[:4] = 0.0
+    for i in range(len(b)):
+        r = b.row(i)
+        g = api.price_american_tc_hedge(r["S0"], r["K"], r["T"], r["sigma"], r["R"], N, r["k"], r["kind"], r["K2"])
+        o = O.price_tc(_opt(r), N)
+        assert g["status"] == o.status == 0
+        assert close(g["ask"], o.ask) and close(g["bid"], o.bid), (i, g, o)
+        for name, gy, oy in (("ask", g["hedge_ask"], o.hedge_ask), ("bid", g["hedge_bid"], o.hedge_bid)):
+            assert abs(gy - oy) <= 1e-8 * (1.0 + abs(oy)), (i, name, gy, oy, r)

@@ -117,3 +117,19 @@ def test_invalid_inputs():
         assert O.price_tc(o, 10).status == O.EINVAL
     # arbitrage: r >= u  (R T/N >= sigma sqrt(T/N))
     assert O.price_tc(O.Option(100.0, 100.0, 1.0, 0.01, 0.5, 0.0), 4).status == O.EARBITRAGE
+
+
+@pytest.mark.parametrize("kind,K,K2", [(O.PUT, 100.0, 0.0), (O.CALL, 95.0, 0.0), (O.BULL, 90.0, 110.0)])
+@pytest.mark.parametrize("N", [3, 40])
+def test_root_hedge_k0_is_crr_delta(kind, K, K2, N):
+    """SURVEY 8(f) NEXT #2 pin (derived A.1): at k = 0 the seller's root hedge is
+    the CRR delta (pi^u - pi^d) / (S0 (u - d)) of the level-1 CRR values, the
+    buyer's its negative."""
+    S0, T, sg, R = 100.0, 1.0, 0.3, 0.05
+    q = O.price_tc(O.Option(S0, K, T, sg, R, 0.0, kind, K2), N)
+    u = math.exp(sg * math.sqrt(T / N))
+    d = 1.0 / u
+    sub = lambda S: O.price_crr(O.Option(S, K, T * (N - 1) / N, sg, R, 0.0, kind, K2), N - 1)
+    delta = (sub(S0 * u) - sub(S0 * d)) / (S0 * (u - d))
+    assert q.hedge_ask == pytest.approx(delta, rel=1e-9, abs=1e-12)
+    assert q.hedge_bid == pytest.approx(-delta, rel=1e-9, abs=1e-12)
