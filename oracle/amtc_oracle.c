@@ -423,7 +423,11 @@ static int buyer_expense(double xi, double zeta, double Sa, double Sb, pwl *out)
 typedef struct {
     double S0, K, K2, T, sigma, R, k;
     int32_t kind;
-    int32_t american; /* 1 = American (default), 0 = European (CRR only) */
+    int32_t american; /* 1 = American (default), 0 = European: no exercise before N
+                         (TC reading: z_t = v_t for t < N) */
+    int32_t cash;     /* 1 = put / call settled in cash ((K-S)^+ or (S-K)^+, 0)
+                         instead of physically (NEXT #3, P:35 settlement-agnostic) */
+    int32_t pad_;
 } or_option;
 
 typedef struct {
@@ -465,8 +469,14 @@ static double node_price(double S0, double u, double d, int t, int j)
 static void payoff(const or_option *o, double S, double *xi, double *zeta)
 {
     switch (o->kind) {
-    case OR_PUT: *xi = o->K; *zeta = -1.0; break;     /* (K, -1) P:94 */
-    case OR_CALL: *xi = -o->K; *zeta = 1.0; break;    /* (-K, +1) */
+    case OR_PUT:
+        if (o->cash) { *xi = fmax(o->K - S, 0.0); *zeta = 0.0; }  /* cash ((K-S)^+, 0) */
+        else { *xi = o->K; *zeta = -1.0; }                          /* (K, -1) P:94 */
+        break;
+    case OR_CALL:
+        if (o->cash) { *xi = fmax(S - o->K, 0.0); *zeta = 0.0; }  /* cash ((S-K)^+, 0) */
+        else { *xi = -o->K; *zeta = 1.0; }                          /* (-K, +1) */
+        break;
     default: /* bull spread, cash */
         *xi = fmax(S - o->K, 0.0) - fmax(S - o->K2, 0.0);
         *zeta = 0.0;
@@ -475,8 +485,9 @@ static void payoff(const or_option *o, double S, double *xi, double *zeta)
 }
 
 /* one node of the seller (party 0) or buyer (party 1) recursion */
-static int node_update(int party, const pwl *zu, const pwl *zd, double r, double Sa, double Sb,
-                       double xi, double zeta, pwl *z, counters *cnt)
+/* exercisable = 0: a European node before expiry, z = v (NEXT #3 reading) */
+static int node_update_x(int party, const pwl *zu, const pwl *zd, double r, double Sa, double Sb,
+                         double xi, double zeta, int exercisable, pwl *z, counters *cnt)
 {
     int st;
     pwl w, f, v, u;
@@ -487,12 +498,19 @@ static int node_update(int party, const pwl *zu, const pwl *zd, double r, double
     st = pwl_restrict(&f, -Sa, -Sb, &v, cnt);                       /* v */
     pwl_free(&f);
     if (st != OR_OK) return st;
+    if (!exercisable) { *z = v; return OR_OK; }
     st = (party == 0) ? seller_expense(xi, zeta, Sa, Sb, &u) : buyer_expense(xi, zeta, Sa, Sb, &u);
     if (st != OR_OK) { pwl_free(&v); return st; }
     st = pwl_envelope(&u, &v, party == 0 ? 1 : 0, z, cnt);          /* max / min (u, v) */
     pwl_free(&u);
     pwl_free(&v);
     return st;
+}
+
+static int node_update(int party, const pwl *zu, const pwl *zd, double r, double Sa, double Sb,
+                       double xi, double zeta, pwl *z, counters *cnt)
+{
+    return node_update_x(party, zu, zd, r, Sa, Sb, xi, zeta, 1, z, cnt);
 }
 
 /*
@@ -541,7 +559,8 @@ int oracle_price_tc(const or_option *o, int N, or_quote *q, int32_t *kinks_out)
                     else q->hedge_bid = bx;
                 }
                 pwl znew;
-                st = node_update(party, &z[party][j], &z[party][j + 1], r, Sa, Sb, xi, zeta, &znew, &cnt);
+                st = node_update_x(party, &z[party][j], &z[party][j + 1], r, Sa, Sb, xi, zeta,
+                                   o->american || t == N, &znew, &cnt);
                 if (st != OR_OK) break;
                 /* z[party][j] is read only by nodes j-1 (done) and j (this one) */
                 pwl_free(&z[party][j]);

@@ -133,3 +133,36 @@ def test_root_hedge_k0_is_crr_delta(kind, K, K2, N):
     delta = (sub(S0 * u) - sub(S0 * d)) / (S0 * (u - d))
     assert q.hedge_ask == pytest.approx(delta, rel=1e-9, abs=1e-12)
     assert q.hedge_bid == pytest.approx(-delta, rel=1e-9, abs=1e-12)
+
+
+@pytest.mark.parametrize("kind,K,K2", [(O.PUT, 100.0, 0.0), (O.CALL, 95.0, 0.0), (O.BULL, 90.0, 110.0)])
+@pytest.mark.parametrize("N", [7, 60])
+def test_european_tc_k0_is_closed_form(kind, K, K2, N):
+    """SURVEY 8(f) NEXT #3 pin: the European transaction-cost recursion (no
+    exercise before N) at k = 0 equals the closed-form binomial sum (A.1 with the
+    early max dropped); ask = bid."""
+    o = O.Option(100.0, K, 0.9, 0.25, 0.04, 0.0, kind, K2, american=False)
+    q = O.price_tc(o, N)
+    ref = O.price_euro_closed(O.Option(100.0, K, 0.9, 0.25, 0.04, 0.0, kind, K2), N)
+    assert q.ask == pytest.approx(ref, rel=1e-10) and q.bid == pytest.approx(ref, rel=1e-10)
+
+
+@pytest.mark.parametrize("kind", [O.PUT, O.CALL])
+def test_cash_settled_k0_is_crr(kind):
+    """NEXT #3 pin: at k = 0 settlement does not matter (A.1): cash = CRR price."""
+    for N in (5, 80):
+        o = O.Option(100.0, 104.0, 0.7, 0.3, 0.05, 0.0, kind, cash=True)
+        q = O.price_tc(o, N)
+        ref = O.price_crr(O.Option(100.0, 104.0, 0.7, 0.3, 0.05, 0.0, kind), N)
+        assert q.ask == pytest.approx(ref, rel=1e-10) and q.bid == pytest.approx(ref, rel=1e-10)
+
+
+@pytest.mark.parametrize("kind", [O.PUT, O.CALL])
+def test_european_below_american_with_costs(kind):
+    """NEXT #3 invariant: fewer exercise rights -- the European ask is at most
+    the American ask and the European bid at most the American bid (k > 0)."""
+    for k in (0.005, 0.02):
+        am = O.price_tc(O.Option(100.0, 100.0, 1.0, 0.2, 0.05, k, kind), 60)
+        eu = O.price_tc(O.Option(100.0, 100.0, 1.0, 0.2, 0.05, k, kind, american=False), 60)
+        assert eu.ask <= am.ask + 1e-12 and eu.bid <= am.bid + 1e-12
+        assert eu.bid <= eu.ask
