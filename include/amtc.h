@@ -31,11 +31,17 @@ typedef enum {
     AMTC_BULL_SPREAD = 2 /* cash: ((S-K)^+ - (S-K2)^+, 0), K < K2 */
 } amtc_kind;
 
+/* payoff flags (amtc_payoff.flags, amtc_batch_soa.flags) */
+enum {
+    AMTC_EUROPEAN = 1u << 0, /* no exercise before N: z_t = v_t for t < N (reading)      */
+    AMTC_CASH = 1u << 1      /* put / call settled in cash: ((K-S)^+, 0) / ((S-K)^+, 0)    */
+};
+
 /* status codes (per option and per call; a call returns the worst status) */
 typedef enum {
     AMTC_OK = 0,
     AMTC_EINVAL = 1,      /* S0, K, T, sigma <= 0; N < 1; k not in [0,1); bull with K >= K2;
-                             unknown kind; null pointer                                     */
+                             unknown kind or flag bit; AMTC_CASH on a bull spread; null pointer */
     AMTC_EARBITRAGE = 2,  /* not d < r < u (risk-neutral p outside (0,1))                   */
     AMTC_ECAPACITY = 3,   /* a node function outgrew every scratch capacity tried           */
     AMTC_EUNBOUNDED = 4,  /* slope restriction infimum is -inf (impossible when d<r<u)      */
@@ -54,7 +60,7 @@ typedef struct {
 /* payoff of one option */
 typedef struct {
     int32_t kind;   /* amtc_kind                                   */
-    uint32_t flags; /* reserved, must be 0                         */
+    uint32_t flags; /* AMTC_EUROPEAN | AMTC_CASH (0: American, physical) */
     double K;       /* strike (bull spread: the long strike K1)    */
     double K2;      /* bull spread: the short strike, > K; else 0  */
 } amtc_payoff;
@@ -79,6 +85,7 @@ typedef struct {
     const double* R;
     const double* k;      /* proportional transaction cost rate, in [0,1); may be NULL for CRR */
     const int32_t* kind;  /* amtc_kind */
+    const uint32_t* flags; /* AMTC_EUROPEAN | AMTC_CASH per option; may be NULL (all 0) */
 } amtc_batch_soa;
 
 /*

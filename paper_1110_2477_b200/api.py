@@ -18,6 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libamtc.so")
 
 PUT, CALL, BULL = 0, 1, 2
+EUROPEAN, CASH = 1, 2  # payoff flags (AMTC_EUROPEAN, AMTC_CASH)
 STATUS = {0: "OK", 1: "EINVAL", 2: "EARBITRAGE", 3: "ECAPACITY", 4: "EUNBOUNDED", 5: "ECUDA", 6: "ENCCL"}
 
 
@@ -35,7 +36,8 @@ class Quote(C.Structure):
 
 class BatchSoA(C.Structure):
     _fields_ = [("S0", C.c_void_p), ("K", C.c_void_p), ("K2", C.c_void_p), ("T", C.c_void_p),
-                ("sigma", C.c_void_p), ("R", C.c_void_p), ("k", C.c_void_p), ("kind", C.c_void_p)]
+                ("sigma", C.c_void_p), ("R", C.c_void_p), ("k", C.c_void_p), ("kind", C.c_void_p),
+                ("flags", C.c_void_p)]
 
 
 class TcStats(C.Structure):
@@ -149,10 +151,10 @@ def tc_last_stats() -> dict:
 # ---------------------------------------------------------------------------
 
 def price_american_tc(S0: float, K: float, T: float, sigma: float, R: float, N: int, k: float,
-                      kind: int = PUT, K2: float = 0.0) -> dict:
-    """Ask and bid of one American option under proportional costs k."""
+                      kind: int = PUT, K2: float = 0.0, flags: int = 0) -> dict:
+    """Ask and bid of one option under proportional costs k (flags: EUROPEAN | CASH)."""
     p = Params(S0, T, sigma, R)
-    y = Payoff(kind, 0, K, K2)
+    y = Payoff(kind, flags, K, K2)
     q = lib().amtc_price_american_tc(C.byref(p), N, C.byref(y), k)
     return {"ask": q.ask, "bid": q.bid, "status": q.status, "max_bp": q.max_bp}
 
@@ -161,7 +163,7 @@ def price_american_tc(S0: float, K: float, T: float, sigma: float, R: float, N: 
 # batches
 # ---------------------------------------------------------------------------
 
-_FIELDS = ("S0", "K", "K2", "T", "sigma", "R", "k", "kind")
+_FIELDS = ("S0", "K", "K2", "T", "sigma", "R", "k", "kind", "flags")
 
 
 def _soa_from_torch(cols: dict) -> BatchSoA:
@@ -176,7 +178,7 @@ def _soa_from_numpy(cols: dict):
         if a is None:
             keep[f] = None
             continue
-        dt = np.int32 if f == "kind" else np.float64
+        dt = np.int32 if f == "kind" else (np.uint32 if f == "flags" else np.float64)
         keep[f] = np.ascontiguousarray(a, dtype=dt)
     soa = BatchSoA(**{f: (keep[f].ctypes.data if keep[f] is not None else None) for f in _FIELDS})
     return soa, keep
@@ -187,7 +189,9 @@ def device_batch(batch, device="cuda"):
     import torch
     out = {}
     for f in _FIELDS:
-        a = getattr(batch, f)
+        a = getattr(batch, f, None)
+        if a is None:
+            continue
         out[f] = torch.from_numpy(np.ascontiguousarray(a)).to(device)
     return out
 
@@ -218,7 +222,7 @@ def quotes_to_numpy(out) -> np.ndarray:
 
 def price_american_tc_batch_host(batch, N: int, stream=None) -> tuple[np.ndarray, int]:
     """Host batch (numpy SoA, e.g. workloads.Batch); H2D/D2H inside the call."""
-    cols = {f: getattr(batch, f) for f in _FIELDS} if not isinstance(batch, dict) else batch
+    cols = {f: getattr(batch, f, None) for f in _FIELDS} if not isinstance(batch, dict) else batch
     soa, keep = _soa_from_numpy(cols)
     n = len(keep["S0"])
     out = np.zeros(n, dtype=QUOTE_DTYPE)
@@ -239,7 +243,7 @@ def price_crr_batch(cols: dict, N: int, out=None, stream=None):
 
 
 def price_crr_batch_host(batch, N: int, stream=None) -> np.ndarray:
-    cols = {f: getattr(batch, f) for f in _FIELDS} if not isinstance(batch, dict) else batch
+    cols = {f: getattr(batch, f, None) for f in _FIELDS} if not isinstance(batch, dict) else batch
     soa, keep = _soa_from_numpy(cols)
     n = len(keep["S0"])
     out = np.zeros(n, dtype=np.float64)

@@ -91,7 +91,7 @@ static DevState* state_for_device(int dev) {
 static BatchPtrs to_ptrs(const amtc_batch_soa* b) {
     BatchPtrs p;
     p.S0 = b->S0; p.K = b->K; p.K2 = b->K2; p.T = b->T;
-    p.sigma = b->sigma; p.R = b->R; p.k = b->k; p.kind = b->kind;
+    p.sigma = b->sigma; p.R = b->R; p.k = b->k; p.kind = b->kind; p.flags = b->flags;
     return p;
 }
 
@@ -402,8 +402,10 @@ int tc_tree_sharded(const void* params_v, int N, const void* payoff_v, double k,
     // one option, host -> device
     double S0 = p->S0, K = y->K, K2 = y->K2, T = p->T, sg = p->sigma, R = p->R, kk = k;
     int32_t kind = y->kind;
+    uint32_t fl = y->flags;
     amtc_batch_soa h;
     h.S0 = &S0; h.K = &K; h.K2 = &K2; h.T = &T; h.sigma = &sg; h.R = &R; h.k = &kk; h.kind = &kind;
+    h.flags = &fl;
     std::lock_guard<std::mutex> guard(st->mu);
     if (!st->sm_count) {
         AMTC_CUDA(cudaDeviceGetAttribute(&st->sm_count, cudaDevAttrMultiProcessorCount, dev));
@@ -531,7 +533,7 @@ int tc_tree_sharded(const void* params_v, int N, const void* payoff_v, double k,
 }
 
 // host-pointer variants: stage through device buffers
-static size_t soa_bytes(int64_t n) { return (size_t)n * (7 * sizeof(double) + sizeof(int32_t)); }
+static size_t soa_bytes(int64_t n) { return (size_t)n * (7 * sizeof(double) + 2 * sizeof(int32_t)); }
 
 static int stage_in(DevState* st, const amtc_batch_soa* h, int64_t n, amtc_batch_soa* d, cudaStream_t s) {
     cudaError_t e = st->stage_in.ensure(soa_bytes(n) + 64);
@@ -557,9 +559,11 @@ static int stage_in(DevState* st, const amtc_batch_soa* h, int64_t n, amtc_batch
             *dst[a] = src[a] ? f + a * n : nullptr;
         }
         std::memcpy(reinterpret_cast<int32_t*>(hf + 7 * n), h->kind, sizeof(int32_t) * n);
+        if (h->flags) std::memcpy(reinterpret_cast<uint32_t*>(hf + 7 * n) + n, h->flags, sizeof(uint32_t) * n);
         AMTC_CUDA(cudaMemcpyAsync(f, hf, need, cudaMemcpyHostToDevice, s));
         AMTC_CUDA(cudaStreamSynchronize(s));  // the pinned buffer is reused by the next call
         d->kind = reinterpret_cast<int32_t*>(f + 7 * n);
+        d->flags = h->flags ? reinterpret_cast<uint32_t*>(f + 7 * n) + n : nullptr;
         return STATUS_OK;
     }
     for (int a = 0; a < 7; ++a) {
@@ -573,6 +577,12 @@ static int stage_in(DevState* st, const amtc_batch_soa* h, int64_t n, amtc_batch
     int32_t* kd = reinterpret_cast<int32_t*>(f + 7 * n);
     AMTC_CUDA(cudaMemcpyAsync(kd, h->kind, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
     d->kind = kd;
+    d->flags = nullptr;
+    if (h->flags) {
+        uint32_t* fd = reinterpret_cast<uint32_t*>(kd + n);
+        AMTC_CUDA(cudaMemcpyAsync(fd, h->flags, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, s));
+        d->flags = fd;
+    }
     return STATUS_OK;
 }
 
@@ -625,14 +635,16 @@ amtc_quote amtc_price_american_tc(const amtc_params* params, int32_t N, const am
     q.ask = NAN;
     q.bid = NAN;
     q.max_bp = 0;
-    if (!params || !payoff || payoff->flags != 0) {
+    if (!params || !payoff) {
         q.status = STATUS_EINVAL;
         return q;
     }
     double S0 = params->S0, K = payoff->K, K2 = payoff->K2, T = params->T, sg = params->sigma, R = params->R;
     int32_t kind = payoff->kind;
+    uint32_t fl = payoff->flags;
     amtc_batch_soa h;
     h.S0 = &S0; h.K = &K; h.K2 = &K2; h.T = &T; h.sigma = &sg; h.R = &R; h.k = &k; h.kind = &kind;
+    h.flags = &fl;
     int rc = amtc_price_american_tc_batch_host(&h, 1, N, &q, nullptr);
     if (rc == STATUS_ECUDA || (rc == STATUS_EINVAL && N < 1)) q.status = rc;
     return q;
@@ -646,12 +658,14 @@ int amtc_price_american_tc_hedge(const amtc_params* params, int32_t N, const amt
         out->max_bp = 0;
         out->status = STATUS_EINVAL;
         *y_ask = *y_bid = NAN;
-        if (!params || !payoff || payoff->flags != 0) return STATUS_EINVAL;
+        if (!params || !payoff) return STATUS_EINVAL;
         double S0 = params->S0, K = payoff->K, K2 = payoff->K2, T = params->T, sg = params->sigma, R = params->R;
         double kk = k;
         int32_t kind = payoff->kind;
+        uint32_t fl = payoff->flags;
         amtc_batch_soa h;
         h.S0 = &S0; h.K = &K; h.K2 = &K2; h.T = &T; h.sigma = &sg; h.R = &R; h.k = &kk; h.kind = &kind;
+        h.flags = &fl;
         cudaStream_t s = nullptr;
         int dev = 0;
         AMTC_CUDA(cudaGetDevice(&dev));

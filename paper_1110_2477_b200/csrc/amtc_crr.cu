@@ -40,7 +40,8 @@ __device__ __forceinline__ double min_nonneg(double a, double b) {
 constexpr int CRR_THREADS = 128;
 
 template <int C, int KIND>
-__device__ __forceinline__ double crr_tree(int lane, int N, double S0, double K, double K2, double h, double rho) {
+__device__ __forceinline__ double crr_tree(int lane, int N, double S0, double K, double K2, double h, double rho,
+                                           bool euro) {
     const double u = exp(h), d = 1.0 / u, r = exp(rho);
     const double p = (r - d) / (u - d);
     const double pu = p / r, pd = (1.0 - p) / r;
@@ -86,7 +87,8 @@ __device__ __forceinline__ double crr_tree(int lane, int N, double S0, double K,
                     ex = x;
                     x = fma(d2, x, c2);
                 }
-                V[c][q] = max_nonneg(ex, fma(pu, V[c][q], pd * vn));
+                const double cont = fma(pu, V[c][q], pd * vn);
+                V[c][q] = euro ? cont : max_nonneg(ex, cont);  // European: no early exercise (NEXT #3)
             }
         }
     }
@@ -104,16 +106,19 @@ __global__ void __launch_bounds__(CRR_THREADS, AMTC_CRR_MINB) crr_kernel(BatchPt
     const double S0 = in.S0[w], K = in.K[w], T = in.T[w], sigma = in.sigma[w], R = in.R[w];
     const double K2 = in.K2 ? in.K2[w] : 0.0;
     const int kind = in.kind[w];
+    const unsigned flags = in.flags ? in.flags[w] : 0u;
+    const bool euro = (flags & FLAG_EUROPEAN) != 0;  // cash settlement: the same CRR value (A.1)
     bool ok = (S0 > 0.0) && (T > 0.0) && (sigma > 0.0) && isfinite(R);
+    ok = ok && !(flags & ~FLAG_ALL) && !((flags & FLAG_CASH) && kind == KIND_BULL);
     ok = ok && (kind == KIND_PUT || kind == KIND_CALL || kind == KIND_BULL);
     ok = ok && (kind == KIND_BULL ? (K < K2) : (K > 0.0));
     const double h = sigma * sqrt(T / (double)N), rho = R * T / (double)N;
     ok = ok && (rho < h) && (-h < rho);  // d < r < u
     double v = NAN;
     if (ok) {  // warp-uniform
-        if (kind == KIND_PUT) v = crr_tree<C, KIND_PUT>(lane, N, S0, K, K2, h, rho);
-        else if (kind == KIND_CALL) v = crr_tree<C, KIND_CALL>(lane, N, S0, K, K2, h, rho);
-        else v = crr_tree<C, KIND_BULL>(lane, N, S0, K, K2, h, rho);
+        if (kind == KIND_PUT) v = crr_tree<C, KIND_PUT>(lane, N, S0, K, K2, h, rho, euro);
+        else if (kind == KIND_CALL) v = crr_tree<C, KIND_CALL>(lane, N, S0, K, K2, h, rho, euro);
+        else v = crr_tree<C, KIND_BULL>(lane, N, S0, K, K2, h, rho, euro);
     }
     if (lane == 0) out[w] = v;
 }

@@ -28,7 +28,9 @@ struct BatchPtrs {
     const double* R;
     const double* k;
     const int32_t* kind;
+    const uint32_t* flags;  // may be null (all 0)
 };
+enum : unsigned { FLAG_EUROPEAN = 1u, FLAG_CASH = 2u, FLAG_ALL = 3u };
 
 // mirrors amtc_quote (24 bytes)
 struct Quote {

@@ -264,7 +264,8 @@ __device__ __noinline__ int root_phase(Fn mine, OptionConsts oc, bool seller, Qu
     if (lane == 0) {
         double xi, zeta;
         option_payoff(oc, oc.S0, xi, zeta);
-        const double intrinsic = xi + zeta * oc.S0;  // u_0(0): S^a_0 = S^b_0 = S0
+        // u_0(0) (S^a_0 = S^b_0 = S0); a European option cannot be exercised at t = 0
+        const double intrinsic = (oc.flags & FLAG_EUROPEAN) ? -INFINITY : xi + zeta * oc.S0;
         if (seller) q->ask = fmax(intrinsic, mv);    // pi^a = z_0(0)
         else q->bid = fmax(intrinsic, -mv);          // pi^b = -z'_0(0)
         if (hedge) *hedge = ymin;                    // the position taken at t = 0 (NEXT #2)
@@ -441,7 +442,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
                 double xi, zeta;
                 option_payoff(oc, S_, xi, zeta);
                 const double ux = seller ? zeta : -zeta;
-                const double uf = (seller ? xi : -xi) * disc;
+                double uf = (seller ? xi : -xi) * disc;
+                // European (NEXT #3): no exercise before N -- u moves out of reach, z = v
+                if ((oc.flags & FLAG_EUROPEAN) && t < N) uf = seller ? -1e300 : 1e300;
 
                 // tier 1 / tier 2: sequential update by this lane (pwl_lane.cuh).
                 // Pass 1 reads the children and leaves A in the lane's scratch

@@ -53,6 +53,7 @@ constexpr int TREE_THREADS = 128;
 struct TreeConsts {
     double S0, K, K2, h, pu, pd, d, c0;
     int kind;
+    int euro;  // European: no early exercise (NEXT #3)
 };
 
 __device__ __forceinline__ double max_nonneg(double x, double c) {  // max(x, c) for c >= +0
@@ -110,7 +111,8 @@ __global__ void __launch_bounds__(TREE_THREADS) tree_band_kernel(TreeConsts c, i
                 X[q] = fma(c.d, X[q], c.c0);
                 ex = X[q];
             }
-            V[q] = max_nonneg(ex, fma(c.pu, V[q], c.pd * vn));
+            const double cont = fma(c.pu, V[q], c.pd * vn);
+            V[q] = c.euro ? cont : max_nonneg(ex, cont);
         }
     }
 #pragma unroll
@@ -125,7 +127,9 @@ __global__ void __launch_bounds__(TREE_THREADS) tree_band_kernel(TreeConsts c, i
 // host side
 // ---------------------------------------------------------------------------
 static int tree_consts(const amtc_params* p, int N, const amtc_payoff* pay, TreeConsts& c) {
-    if (!p || !pay || pay->flags != 0 || N < 1) return STATUS_EINVAL;
+    if (!p || !pay || (pay->flags & ~3u) || N < 1) return STATUS_EINVAL;
+    if ((pay->flags & 2u) && pay->kind == KIND_BULL) return STATUS_EINVAL;  // AMTC_CASH: put / call only
+    c.euro = (pay->flags & 1u) ? 1 : 0;  // AMTC_EUROPEAN (cash settlement: the same CRR value, A.1)
     if (!(p->S0 > 0.0) || !(p->T > 0.0) || !(p->sigma > 0.0) || !std::isfinite(p->R)) return STATUS_EINVAL;
     c.kind = pay->kind;
     c.S0 = p->S0;
@@ -351,7 +355,7 @@ int amtc_price_tree_sharded(const amtc_params* params, int32_t N, const amtc_pay
                 *out = amtc_price_american_tc(params, N, payoff, k);
                 return out->status;
             }
-            if (!params || !payoff || payoff->flags != 0) return STATUS_EINVAL;
+            if (!params || !payoff) return STATUS_EINVAL;
             if (N < 64) {  // too small to shard: every rank prices it alone
                 *out = amtc_price_american_tc(params, N, payoff, k);
                 return out->status;

@@ -55,7 +55,7 @@ def test_strerror_without_gpu(lib):
 def test_quote_layout():
     from paper_1110_2477_b200 import api
     assert ctypes.sizeof(api.Quote) == 24
-    assert ctypes.sizeof(api.BatchSoA) == 8 * 8
+    assert ctypes.sizeof(api.BatchSoA) == 9 * 8
 
 
 def test_product_package_never_imports_oracle():
