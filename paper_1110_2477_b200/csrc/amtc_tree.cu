@@ -208,7 +208,16 @@ static TreeBufs* tree_bufs() {
 
 // rank g's columns of a level of width w over n ranks: [a_g, a_{g+1}),
 // a_g = ceil(g w / n) (rank 0 keeps the root column)
-static inline int64_t split_at(int64_t w, int g, int n) { return (g * w + n - 1) / n; }
+// Processor reduction: a level of w columns is spread over
+// n_act = clamp(w / TREE_MIN_COLS, 1, n) ranks only -- small levels near the root
+// stay on rank 0 and the rest drop out instead of exchanging halos for a few
+// columns each.  Rank g < n_act owns [ceil(g w / n_act), ceil((g+1) w / n_act)).
+constexpr int64_t TREE_MIN_COLS = 4096;
+static inline int64_t split_at(int64_t w, int g, int n) {
+    const int64_t na = std::max<int64_t>(1, std::min<int64_t>(n, w / TREE_MIN_COLS));
+    if (g >= na) return w;
+    return (g * w + na - 1) / na;
+}
 
 static thread_local std::string t_err;
 static int cuda_err(cudaError_t e, const char* what) {

@@ -5,7 +5,7 @@ import torch
 from paper_1110_2477_b200 import api, build, workloads as W
 build.build(); api.lib()
 r = W.config5a().row(0)
-for N in (1000, 10000, 100000):
+for N in (1000, 10000, 100000, 1000000):
     api.price_crr_tree(r["S0"], r["K"], r["T"], r["sigma"], r["R"], N)
     ts = []
     for _ in range(5):

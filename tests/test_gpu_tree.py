@@ -94,3 +94,13 @@ def test_sharded_one_rank_nccl(api):
     # several ranks need a communicator
     q = api.price_tree_sharded(100.0, 100.0, 1.0, 0.3, 0.05, 300, 0.005, O.PUT, comm=None, rank=0, nranks=2)
     assert q["status"] == 1 and math.isnan(q["ask"])
+
+
+def test_very_long_tree_1e6(api):
+    """a very-long-dated k=0 tree, N = 10^6 (8 MB level,
+    7813 bands), converges to the paper's 13.906 (reading A16) and agrees
+    with N = 40000 to the paper's 3 decimals."""
+    a = W.appendix_put().row(0)
+    g6 = api.price_crr_tree(a["S0"], a["K"], a["T"], a["sigma"], a["R"], 1_000_000, O.PUT)
+    g4 = api.price_crr_tree(a["S0"], a["K"], a["T"], a["sigma"], a["R"], 40_000, O.PUT)
+    assert abs(g6 - 13.906) <= 5e-4 and abs(g6 - g4) <= 5e-4, (g6, g4)
