@@ -159,8 +159,9 @@ int amtc_comm_destroy(void* comm);
 
 /*
  * One tree sharded over the nranks GPUs of an amtc_comm_init communicator
- * (SURVEY 8(e), config 5): every rank calls it with the same arguments.  Rank
- * g owns columns [ceil(g w/n), ceil((g+1) w/n)) of the current level (w = t+1),
+ * (SURVEY 8(e), config 5): every rank calls it with the same arguments.  k = 0:
+ * rank g owns columns [ceil(g w/na), ceil((g+1) w/na)) of the current level
+ * (w = t+1) on the first na = clamp(w/4096, 1, nranks) ranks,
  * re-split every band of 128 levels (the paper's per-round rebalancing,
  * P:178); before each band the ranks exchange their window halos with
  * ncclSend/ncclRecv (region-B dependency).  k > 0: the tree's

@@ -24,7 +24,8 @@
 // pipe's slow DMNMX (4.0e12/s vs 1.8e13/s DFMA on B200, profiles/r01_fp64_peak.json).
 //
 // Sharding (amtc_price_tree_sharded): rank g owns columns
-// [ceil(g w / n), ceil((g+1) w / n)) of the current level (w = t + 1 columns,
+// [ceil(g w / n_a), ceil((g+1) w / n_a)) of the current level (w = t + 1 columns,
+// n_a = clamp(w / 4096, 1, n) active ranks: processor reduction, P:286-288;
 // re-split every band -- the paper's per-round rebalancing).  Before a
 // band each rank gathers its input window from the owners (ncclSend/ncclRecv
 // in one group: its own range plus a halo of D columns from the right and the
