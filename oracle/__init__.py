@@ -48,7 +48,7 @@ def build(force: bool = False) -> str:
 class _Option(C.Structure):
     _fields_ = [("S0", C.c_double), ("K", C.c_double), ("K2", C.c_double), ("T", C.c_double),
                 ("sigma", C.c_double), ("R", C.c_double), ("k", C.c_double),
-                ("kind", C.c_int32), ("american", C.c_int32), ("cash", C.c_int32), ("pad_", C.c_int32)]
+                ("kind", C.c_int32), ("american", C.c_int32), ("cash", C.c_int32), ("cost_t0", C.c_int32)]
 
 
 class _Quote(C.Structure):
@@ -93,10 +93,11 @@ class Option:
     K2: float = 0.0
     american: bool = True
     cash: bool = False
+    cost_t0: bool = False
 
     def _c(self) -> _Option:
         return _Option(self.S0, self.K, self.K2, self.T, self.sigma, self.R, self.k, self.kind,
-                       1 if self.american else 0, 1 if self.cash else 0, 0)
+                       1 if self.american else 0, 1 if self.cash else 0, 1 if self.cost_t0 else 0)
 
 
 @dataclass

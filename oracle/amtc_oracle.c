@@ -427,7 +427,8 @@ typedef struct {
                          (TC reading: z_t = v_t for t < N) */
     int32_t cash;     /* 1 = put / call settled in cash ((K-S)^+ or (S-K)^+, 0)
                          instead of physically (NEXT #3, P:35 settlement-agnostic) */
-    int32_t pad_;
+    int32_t cost_t0;  /* 1 = proportional costs also at t = 0 (variant of P:159's
+                         convention, NEXT #3): S^a_0 = (1+k) S0, S^b_0 = (1-k) S0 */
 } or_option;
 
 typedef struct {
@@ -523,6 +524,7 @@ int oracle_price_tc(const or_option *o, int N, or_quote *q, int32_t *kinks_out)
     double u, d, r;
     memset(q, 0, sizeof *q);
     q->ask = q->bid = NAN;
+    q->hedge_ask = q->hedge_bid = NAN;
     int st = calibrate(o, N, &u, &d, &r);
     if (st != OR_OK) { q->status = st; return st; }
     counters cnt = {0, 0};
@@ -540,12 +542,12 @@ int oracle_price_tc(const or_option *o, int N, or_quote *q, int32_t *kinks_out)
         for (int j = 0; j <= t && st == OR_OK; j++) {
             double S = node_price(o->S0, u, d, t, j);
             double Sa, Sb;
-            if (t == 0) { Sa = Sb = S; } /* no costs at t = 0 */
+            if (t == 0 && !o->cost_t0) { Sa = Sb = S; } /* no costs at t = 0 */
             else { Sa = (1.0 + o->k) * S; Sb = (1.0 - o->k) * S; }
             double xi, zeta;
             payoff(o, S, &xi, &zeta);
             for (int party = 0; party < 2 && st == OR_OK; party++) {
-                if (t == 0) {
+                if (t == 0 && !o->cost_t0) {
                     /* root hedge: argmin over the vertices of w_0 of w_0(x)/r + S0 x (A.4) */
                     pwl w;
                     if ((st = pwl_envelope(&z[party][0], &z[party][1], 1, &w, &cnt)) != OR_OK) break;

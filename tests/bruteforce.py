@@ -48,7 +48,7 @@ def _payoff(kind, K, K2, S):
     return max(S - K, 0.0) - max(S - K2, 0.0), 0.0
 
 
-def _tree(S0, T, sigma, R, k, N):
+def _tree(S0, T, sigma, R, k, N, cost_t0=False):
     u = math.exp(sigma * math.sqrt(T / N))
     d = 1.0 / u
     r = math.exp(R * T / N)
@@ -63,7 +63,7 @@ def _tree(S0, T, sigma, R, k, N):
     quotes = []
     for (t, m, _, _) in nodes:
         S = S0 * u ** m
-        if t == 0:
+        if t == 0 and not cost_t0:  # no costs at t = 0 unless the variant asks for them
             quotes.append((S, S0, S0))
         else:
             quotes.append((S, (1 + k) * S, (1 - k) * S))
@@ -138,8 +138,8 @@ def _solve(nodes, quotes, r, N, cover_rows):
     return res.fun
 
 
-def ask_lp(S0, K, T, sigma, R, k, N, kind=PUT, K2=0.0):
-    nodes, quotes, r = _tree(S0, T, sigma, R, k, N)
+def ask_lp(S0, K, T, sigma, R, k, N, kind=PUT, K2=0.0, cost_t0=False):
+    nodes, quotes, r = _tree(S0, T, sigma, R, k, N, cost_t0)
     cover = {}
     for i, (t, m, parent, path) in enumerate(nodes):
         cover[i] = (0.0, 0.0) if t == N + 1 else _payoff(kind, K, K2, quotes[i][0])
@@ -222,8 +222,8 @@ def _stopping_times(nodes, N):
     return list(rec(0))
 
 
-def bid_enum(S0, K, T, sigma, R, k, N, kind=PUT, K2=0.0):
-    nodes, quotes, r = _tree(S0, T, sigma, R, k, N)
+def bid_enum(S0, K, T, sigma, R, k, N, kind=PUT, K2=0.0, cost_t0=False):
+    nodes, quotes, r = _tree(S0, T, sigma, R, k, N, cost_t0)
     best = -math.inf
     for tau in _stopping_times(nodes, N):
         cover = {}

@@ -51,3 +51,22 @@ def test_ask_lp_n4():
         q = O.price_tc(O.Option(S0, K, T, sigma, R, 0.01, kind, K2), 4)
         ask = B.ask_lp(S0, K, T, sigma, R, 0.01, 4, kind, K2)
         assert abs(q.ask - ask) <= 1e-8 * max(1.0, abs(ask))
+
+
+@pytest.mark.parametrize("N", [1, 2])
+@pytest.mark.parametrize("k", [0.005, 0.02, 0.1])
+@pytest.mark.parametrize("m", [0, 1, 2, 3])
+def test_cost_at_t0_matches_lp(m, k, N):
+    """SURVEY 8(f) NEXT #3 variant: proportional costs also at t = 0 (quotes
+    (1 +- k) S0 at the root instead of P:159's S0), pinned to the superhedging
+    LP / stopping-time definition with the same root quotes."""
+    S0, K, K2, T, sigma, R, kind = MARKETS[m]
+    q = O.price_tc(O.Option(S0, K, T, sigma, R, k, kind, K2, cost_t0=True), N)
+    assert q.status == 0
+    ask = B.ask_lp(S0, K, T, sigma, R, k, N, kind, K2, cost_t0=True)
+    bid = B.bid_enum(S0, K, T, sigma, R, k, N, kind, K2, cost_t0=True)
+    scale = max(1.0, abs(ask))
+    assert abs(q.ask - ask) <= 1e-7 * scale, (q.ask, ask)
+    assert abs(q.bid - bid) <= 1e-7 * scale, (q.bid, bid)
+    base = O.price_tc(O.Option(S0, K, T, sigma, R, k, kind, K2), N)
+    assert q.ask >= base.ask - 1e-12 and q.bid <= base.bid + 1e-12  # costs at t=0 only widen the spread
