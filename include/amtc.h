@@ -33,8 +33,10 @@ typedef enum {
 
 /* payoff flags (amtc_payoff.flags, amtc_batch_soa.flags) */
 enum {
-    AMTC_EUROPEAN = 1u << 0, /* no exercise before N: z_t = v_t for t < N (reading)      */
-    AMTC_CASH = 1u << 1      /* put / call settled in cash: ((K-S)^+, 0) / ((S-K)^+, 0)    */
+    AMTC_EUROPEAN = 1u << 0,   /* no exercise before N: z_t = v_t for t < N (reading A21)  */
+    AMTC_CASH = 1u << 1,       /* put / call settled in cash: ((K-S)^+, 0) / ((S-K)^+, 0)  */
+    AMTC_COST_AT_T0 = 1u << 2  /* costs also at t = 0: quotes (1 +- k) S0 instead of S0
+                                  (P:159's convention is the default); no root hedge     */
 };
 
 /* status codes (per option and per call; a call returns the worst status) */
@@ -60,7 +62,7 @@ typedef struct {
 /* payoff of one option */
 typedef struct {
     int32_t kind;   /* amtc_kind                                   */
-    uint32_t flags; /* AMTC_EUROPEAN | AMTC_CASH (0: American, physical) */
+    uint32_t flags; /* AMTC_EUROPEAN | AMTC_CASH | AMTC_COST_AT_T0 (0: American, physical) */
     double K;       /* strike (bull spread: the long strike K1)    */
     double K2;      /* bull spread: the short strike, > K; else 0  */
 } amtc_payoff;
@@ -85,7 +87,7 @@ typedef struct {
     const double* R;
     const double* k;      /* proportional transaction cost rate, in [0,1); may be NULL for CRR */
     const int32_t* kind;  /* amtc_kind */
-    const uint32_t* flags; /* AMTC_EUROPEAN | AMTC_CASH per option; may be NULL (all 0) */
+    const uint32_t* flags; /* AMTC_EUROPEAN | AMTC_CASH | AMTC_COST_AT_T0 per option; may be NULL */
 } amtc_batch_soa;
 
 /*

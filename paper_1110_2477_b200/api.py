@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libamtc.so")
 
 PUT, CALL, BULL = 0, 1, 2
-EUROPEAN, CASH = 1, 2  # payoff flags (AMTC_EUROPEAN, AMTC_CASH)
+EUROPEAN, CASH, COST_AT_T0 = 1, 2, 4  # payoff flags (AMTC_EUROPEAN, AMTC_CASH, AMTC_COST_AT_T0)
 STATUS = {0: "OK", 1: "EINVAL", 2: "EARBITRAGE", 3: "ECAPACITY", 4: "EUNBOUNDED", 5: "ECUDA", 6: "ENCCL"}
 
 

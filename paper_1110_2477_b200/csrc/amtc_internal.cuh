@@ -30,7 +30,7 @@ struct BatchPtrs {
     const int32_t* kind;
     const uint32_t* flags;  // may be null (all 0)
 };
-enum : unsigned { FLAG_EUROPEAN = 1u, FLAG_CASH = 2u, FLAG_ALL = 3u };
+enum : unsigned { FLAG_EUROPEAN = 1u, FLAG_CASH = 2u, FLAG_COST_T0 = 4u, FLAG_ALL = 7u };
 
 // mirrors amtc_quote (24 bytes)
 struct Quote {

@@ -257,18 +257,24 @@ __device__ __noinline__ bool serve_one(CtaHdr& H, StripSmem<C, B, true>* all, in
 // over the vertices b of w_0 = max(z_{1,0}, z_{1,1}); returns the status bits.
 __device__ __noinline__ int root_phase(Fn mine, OptionConsts oc, bool seller, Quote* q, double* hedge, int lane) {
     const Fn Ur = shfl_fn(mine, 0), Dr = shfl_fn(mine, 1);
+    // quotes at t = 0: S0 both ways, or (1 +- k) S0 with AMTC_COST_AT_T0 (NEXT #3)
+    const bool c0 = (oc.flags & FLAG_COST_T0) != 0;
+    const double lo = c0 ? -(1.0 + oc.k) * oc.S0 : -oc.S0, hi = c0 ? -(1.0 - oc.k) * oc.S0 : -oc.S0;
     double slW, srW, ymin;
-    const double mv = heavy::root_min(Ur, Dr, oc.S0, slW, srW, ymin, lane);
-    // the minimum exists iff w_0 + S0 y has a decreasing left and increasing right tail
-    if (!(slW + oc.S0 < 0.0) || !(srW + oc.S0 > 0.0)) return DEV_UNBOUNDED;
+    const double v0 = heavy::root_min(Ur, Dr, lo, hi, slW, srW, ymin, lane);
+    // the infimum is finite iff W - hi y decreases on the left and W - lo y increases on the right
+    if (!(slW - hi < 0.0) || !(srW - lo > 0.0)) return DEV_UNBOUNDED;
     if (lane == 0) {
         double xi, zeta;
         option_payoff(oc, oc.S0, xi, zeta);
-        // u_0(0) (S^a_0 = S^b_0 = S0); a European option cannot be exercised at t = 0
-        const double intrinsic = (oc.flags & FLAG_EUROPEAN) ? -INFINITY : xi + zeta * oc.S0;
-        if (seller) q->ask = fmax(intrinsic, mv);    // pi^a = z_0(0)
-        else q->bid = fmax(intrinsic, -mv);          // pi^b = -z'_0(0)
-        if (hedge) *hedge = ymin;                    // the position taken at t = 0 (NEXT #2)
+        // u_0(0) of the seller (vertex (zeta, xi)) / buyer (vertex (-zeta, -xi)), slopes lo | hi;
+        // a European option cannot be exercised at t = 0
+        const double ua = xi + (0.0 < zeta ? lo : hi) * (0.0 - zeta);
+        const double ub = -xi + (0.0 < -zeta ? lo : hi) * (0.0 + zeta);
+        const bool euro = (oc.flags & FLAG_EUROPEAN) != 0;
+        if (seller) q->ask = euro ? v0 : fmax(ua, v0);    // pi^a = z_0(0)
+        else q->bid = -(euro ? v0 : fmin(ub, v0));        // pi^b = -z'_0(0)
+        if (hedge) *hedge = c0 ? NAN : ymin;              // the position taken at t = 0 (NEXT #2)
     }
     return DEV_OK;
 }

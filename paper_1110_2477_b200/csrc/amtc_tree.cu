@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(TREE_THREADS) tree_band_kernel(TreeConsts c, i
 // host side
 // ---------------------------------------------------------------------------
 static int tree_consts(const amtc_params* p, int N, const amtc_payoff* pay, TreeConsts& c) {
-    if (!p || !pay || (pay->flags & ~3u) || N < 1) return STATUS_EINVAL;
+    if (!p || !pay || (pay->flags & ~7u) || N < 1) return STATUS_EINVAL;  // cost-at-t0: no effect at k = 0
     if ((pay->flags & 2u) && pay->kind == KIND_BULL) return STATUS_EINVAL;  // AMTC_CASH: put / call only
     c.euro = (pay->flags & 1u) ? 1 : 0;  // AMTC_EUROPEAN (cash settlement: the same CRR value, A.1)
     if (!(p->S0 > 0.0) || !(p->T > 0.0) || !(p->sigma > 0.0) || !std::isfinite(p->R)) return STATUS_EINVAL;

@@ -1202,20 +1202,34 @@ __device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo,
     return DEV_OK;
 }
 
-// a6 helper: min over the vertices b of W = max(U, D) of W(b) + S0 b, and W's
-// tail slopes (for the boundedness check)
-// (also the minimiser: the root hedge y*, smallest x on ties)
-__device__ __noinline__ double root_min(const Fn U, const Fn D, double S0, double& slW, double& srW, double& ymin,
-                                        int lane) {
+// a6 helper: the value at y = 0 of the restriction of W = max(U, D) to slopes
+// [lo, hi] (t = 0; lo = hi = -S0 without costs at t = 0):
+//   v_0(0) = min( W(0), min_{x_j >= 0} W_j - lo x_j, min_{x_j <= 0} W_j - hi x_j )
+// (buying up to a position x_j >= 0 at the ask -lo, selling down at the bid -hi;
+// infima of PWL functions over half lines sit at 0 or at vertices).  Also W's
+// tail slopes (boundedness) and the minimising vertex (the root hedge, smallest
+// x on ties).
+__device__ __noinline__ double root_min(const Fn U, const Fn D, double lo, double hi, double& slW, double& srW,
+                                        double& ymin, int lane) {
     const HCtx h = make_ctx(U, D);
     const int nb = (h.nE + 31) / 32;
-    double mv = INFINITY, mx = INFINITY;
+    double mv = INFINITY, mx = INFINITY;    // best vertex value and position
+    double lx = -INFINITY, lval = INFINITY;  // the last vertex at or left of 0: W(0) from its right piece
+    double fx = INFINITY, fval = 0.0;       // the first vertex (W(0) from the left tail if none <= 0)
     for (int blk = 0; blk < nb; ++blk) {
         const BlockW B = block_w(h, blk, lane);
         for (int q = 0; q < B.w.n; ++q) {
             const WV w = B.w.get(q);
-            const double g = fma(S0, w.x, w.f);
-            if (g < mv || (g == mv && w.x < mx)) { mv = g; mx = w.x; }
+            if (w.x >= 0.0) {
+                const double g = fma(-lo, w.x, w.f);
+                if (g < mv || (g == mv && w.x < mx)) { mv = g; mx = w.x; }
+            }
+            if (w.x <= 0.0) {
+                const double g = fma(-hi, w.x, w.f);
+                if (g < mv || (g == mv && w.x < mx)) { mv = g; mx = w.x; }
+                if (w.x > lx) { lx = w.x; lval = fma(w.sR, -w.x, w.f); }
+            }
+            if (w.x < fx) { fx = w.x; fval = fma(w.sL, -w.x, w.f); }
         }
     }
     slW = h.tailL_U ? U.sl : D.sl;
@@ -1224,8 +1238,14 @@ __device__ __noinline__ double root_min(const Fn U, const Fn D, double S0, doubl
     for (int o = 16; o > 0; o >>= 1) {
         const double ov = __shfl_xor_sync(FULLM, mv, o), ox = __shfl_xor_sync(FULLM, mx, o);
         if (ov < mv || (ov == mv && ox < mx)) { mv = ov; mx = ox; }
+        const double olx = __shfl_xor_sync(FULLM, lx, o), olv = __shfl_xor_sync(FULLM, lval, o);
+        if (olx > lx) { lx = olx; lval = olv; }
+        const double ofx = __shfl_xor_sync(FULLM, fx, o), ofv = __shfl_xor_sync(FULLM, fval, o);
+        if (ofx < fx) { fx = ofx; fval = ofv; }
     }
+    const double w0 = (lx > -INFINITY) ? lval : fval;  // W(0)
     ymin = mx;
+    if (w0 < mv) { mv = w0; ymin = 0.0; }
     return mv;
 }
 

@@ -335,13 +335,14 @@ def test_root_hedge(api, N):
 
 @pytest.mark.parametrize("N", [9, 120])
 def test_european_and_cash_variants(api, N):
-    """European (no exercise before N) and cash-settled
-    put / call variants through the batch flags, against the oracle's variants
-    (pinned to the closed-form sum and to CRR at k = 0 in test_oracle_identities.py)."""
+    """European (no exercise before N), cash-settled put /
+    call and costs-at-t=0 variants through the batch flags, against the oracle's
+    variants (pinned to the closed-form sum and CRR at k = 0, and to the LP brute
+    force for costs at t = 0)."""
     b = W.random_small(40, seed=8000 + N, k_max=0.03)
     rng = np.random.default_rng(N)
-    flags = rng.integers(0, 4, len(b)).astype(np.uint32)
-    flags[b.kind == 2] &= 1  # cash settlement is for puts and calls (bull spreads are cash already)
+    flags = rng.integers(0, 8, len(b)).astype(np.uint32)  # EUROPEAN | CASH | COST_AT_T0
+    flags[b.kind == 2] &= 5  # cash settlement is for puts and calls (bull spreads are cash already)
     cols = {f: getattr(b, f) for f in W.Batch.fields()}
     cols["flags"] = flags
     got, rc = api.price_american_tc_batch_host(cols, N)
@@ -350,7 +351,8 @@ def test_european_and_cash_variants(api, N):
     for i in range(len(b)):
         r = b.row(i)
         want.append(O.price_tc(O.Option(r["S0"], r["K"], r["T"], r["sigma"], r["R"], r["k"], r["kind"], r["K2"],
-                                        american=not (flags[i] & 1), cash=bool(flags[i] & 2)), N))
+                                        american=not (flags[i] & 1), cash=bool(flags[i] & 2),
+                                        cost_t0=bool(flags[i] & 4)), N))
     assert_quotes(got, b, N, want)
     # k = 0 CRR kernels: European / cash on the batch CRR path and the single-tree path
     crr = api.price_crr_batch_host(cols, N)
@@ -361,6 +363,6 @@ def test_european_and_cash_variants(api, N):
         assert close(crr[i], o), (i, crr[i], o)
     # invalid: cash on a bull spread, unknown bit
     bad = dict(cols)
-    bad["flags"] = np.where(b.kind == 2, 2, 8).astype(np.uint32)
+    bad["flags"] = np.where(b.kind == 2, 2, 16).astype(np.uint32)
     q, rc = api.price_american_tc_batch_host(bad, N)
     assert rc == 1 and np.all(q["status"] == 1)
