@@ -352,7 +352,6 @@ def run_tree(args):
     split mode) on rank 0.  Timer: host wall clock around the synchronous C-ABI
     calls (they include the host-side band loop), max over ranks."""
     import torch
-    import oracle as O_  # cpu_baseline leg only
     from paper_1110_2477_b200 import api, build, workloads as W
     world, rank, local, pg = setup_dist()
     assert torch.cuda.is_available(), "bench.py needs a CUDA device"
@@ -373,7 +372,7 @@ def run_tree(args):
         nodes = crr_nodes(N)
         desc = f"config5a: one American put tree, k=0 CRR, N={N}, sharded over {world} GPU(s) (NCCL halo per band)"
         scaling = "strong"
-        cpu_sample = (O_.Option(r["S0"], r["K"], r["T"], r["sigma"], r["R"], 0.0, O_.PUT), 20000, "crr")
+        cpu_sample = (dict(S0=r["S0"], K=r["K"], T=r["T"], sigma=r["sigma"], R=r["R"], k=0.0, kind=0), 20000, "crr")
     else:
         if args.config == 1:
             trees = [(W.config1().row(0), W.CONFIG1_N)]
@@ -401,8 +400,8 @@ def run_tree(args):
         nodes = sum(tc_nodes(N_) for _, N_ in trees)
         scaling = "weak"
         row0, N0 = trees[0]
-        cpu_sample = (O_.Option(row0["S0"], row0["K"], row0["T"], row0["sigma"], row0["R"], row0["k"], row0["kind"],
-                                row0["K2"]), N0, "tc")
+        cpu_sample = (dict(S0=row0["S0"], K=row0["K"], T=row0["T"], sigma=row0["sigma"], R=row0["R"], k=row0["k"],
+                           kind=row0["kind"], K2=row0["K2"]), N0, "tc")
         N = max(N_ for _, N_ in trees)
     for _ in range(args.warmup):
         step()
@@ -446,7 +445,9 @@ def run_tree(args):
                               "ask": q5["ask"], "bid": q5["bid"]}}
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        opt, Ns, kind = cpu_sample
+        import oracle as O_  # the cpu_baseline leg only
+        params, Ns, kind = cpu_sample
+        opt = O_.Option(**params)
         t0 = time.perf_counter()
         if kind == "crr":
             O_.price_crr(opt, Ns)
