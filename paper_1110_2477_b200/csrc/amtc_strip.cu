@@ -165,6 +165,36 @@ struct StripLaunch {
 #define WS(T, field, q) reinterpret_cast<T*>(wb + L.lay.field + (size_t)(q) * L.lay.field##_ps)
 #define WS1(T, field) reinterpret_cast<T*>(wb + L.lay.field)
 
+// carry-column pointers of strip s (out) or of the strip to its right (in),
+// rebuilt at each use from the launch parameters instead of being kept live
+// across the level loop (register pressure: the loop state spills otherwise)
+struct CarryPtrs {
+    int2* chdr;
+    double* csl;
+    Vtx* cv;
+    Vtx* ca;
+};
+__device__ __forceinline__ CarryPtrs carry_ptrs(const StripLaunch& L, char* wb, int tree, int s, bool split,
+                                                bool input) {
+    CarryPtrs P;
+    if (split) {
+        const bool remote = input && s + 1 == L.peer_strip;
+        const size_t si = (size_t)tree * L.split_S + s + (input ? 1 : 0);
+        char* c = (remote ? L.peer_carry : L.carry) + si * L.carry_stride;
+        P.chdr = reinterpret_cast<int2*>(c);
+        P.csl = reinterpret_cast<double*>(c + L.c_csl);
+        P.cv = reinterpret_cast<Vtx*>(c + L.c_cv);
+        P.ca = (remote ? L.peer_carena : L.carena_split) + (size_t)tree * L.carena_split_cap;
+    } else {
+        const int q = (s & 1) ^ (input ? 1 : 0);
+        P.chdr = reinterpret_cast<int2*>(wb + L.lay.chdr + (size_t)q * L.lay.chdr_ps);
+        P.csl = reinterpret_cast<double*>(wb + L.lay.csl + (size_t)q * L.lay.csl_ps);
+        P.cv = reinterpret_cast<Vtx*>(wb + L.lay.cv + (size_t)q * L.lay.cv_ps);
+        P.ca = reinterpret_cast<Vtx*>(wb + L.lay.carena + (size_t)q * L.lay.carena_ps);
+    }
+    return P;
+}
+
 // copy n vertices between (possibly strided) locations, one lane
 __device__ __forceinline__ void copy_fn(Vtx* dst, int dstride, const Vtx* src, int sstride, int n) {
     for (int i = 0; i < n; ++i) dst[i * dstride] = src[i * sstride];
@@ -288,10 +318,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
     StripSmem<C, B, HEAVY>& S = all[wib];
     const int N = L.N;
     char* const wb = L.ws + (size_t)(blockIdx.x * WARPS + wib) * L.lay.total;
-    double* const Epow = WS1(double, epow);
-    double* const Dpow = WS1(double, dpow);
-    Vtx* const hscr = WS1(Vtx, hscr);
-    Vtx* const zbuf = WS1(Vtx, zbuf);
+#define Epow WS1(double, epow)
+#define Dpow WS1(double, dpow)
+#define hscr WS1(Vtx, hscr)
+#define zbuf WS1(Vtx, zbuf)
     if (threadIdx.x == 0) {
         H.active = WARPS;
         H.posted = 0;
@@ -330,52 +360,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
 
         for (int s = s_first; s >= s_last && !err; --s) {
             const int j0 = s * SW, j = j0 + lane;
-            const int cout = s & 1, cin = cout ^ 1;
-            // carry columns: this strip's (out) and the strip to the right's (in)
-            int2* chdr_o;
-            double* csl_o;
-            Vtx* cv_o;
-            Vtx* ca_o;
-            int* ccnt;
-            int ccap;
-            const int2* chdr_i;
-            const double* csl_i;
-            const Vtx* cv_i;
-            const Vtx* ca_i;
-            volatile int* prog_in = nullptr;
-            volatile int* prog_out = nullptr;
-            if (split) {
-                // strip s+1 may live on the next GPU (sharded tree): its carry
-                // column, carry arena and progress counter are then read through
-                // the peer's memory (CUDA IPC over NVLink)
-                const bool remote = s + 1 == L.peer_strip;
-                const size_t si = (size_t)tree * L.split_S + s;
-                char* co = L.carry + si * L.carry_stride;
-                char* ci = (remote ? L.peer_carry : L.carry) + (si + 1) * L.carry_stride;
-                chdr_o = reinterpret_cast<int2*>(co);
-                csl_o = reinterpret_cast<double*>(co + L.c_csl);
-                cv_o = reinterpret_cast<Vtx*>(co + L.c_cv);
-                chdr_i = reinterpret_cast<const int2*>(ci);
-                csl_i = reinterpret_cast<const double*>(ci + L.c_csl);
-                cv_i = reinterpret_cast<const Vtx*>(ci + L.c_cv);
-                ca_o = L.carena_split + (size_t)tree * L.carena_split_cap;
-                ca_i = (remote ? L.peer_carena : L.carena_split) + (size_t)tree * L.carena_split_cap;
-                ccnt = &L.carena_cnt[tree];
-                ccap = L.carena_split_cap;
-                prog_out = L.progress + si;
-                prog_in = (remote ? L.peer_progress : L.progress) + si + 1;
-            } else {
-                chdr_o = WS(int2, chdr, cout);
-                csl_o = WS(double, csl, cout);
-                cv_o = WS(Vtx, cv, cout);
-                ca_o = WS(Vtx, carena, cout);
-                chdr_i = WS(int2, chdr, cin);
-                csl_i = WS(double, csl, cin);
-                cv_i = WS(Vtx, cv, cin);
-                ca_i = WS(Vtx, carena, cin);
-                ccnt = &S.ccnt;
-                ccap = L.caps.carena_cap;
-            }
+            // split mode: progress counters of this strip and of the strip to its right
+            volatile int* const prog_out = split ? L.progress + (size_t)tree * L.split_S + s : nullptr;
             // a2: leaves t = N+1, payoff (0,0): z = y^- S^a - y^+ S^b
             int my_n = 0, my_off = -1;
             double my_sl = 0.0;
@@ -424,7 +410,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
                     D = make_fn(&S.leaf31, 1, leaf31_sl, 1);  // the analytic leaf (N+1, j+1)
                 } else if (active) {
                     int pv = 0;
-                    if (prog_in) {  // split mode: wait until strip s+1 has published level t+1
+                    if (split) {  // split mode: wait until strip s+1 has published level t+1
+                        const bool remote = s + 1 == L.peer_strip;
+                        volatile int* const prog_in =
+                            (remote ? L.peer_progress : L.progress) + (size_t)tree * L.split_S + s + 1;
                         while ((pv = *prog_in) > t + 1) __nanosleep(32);
                         __threadfence();
                     }
@@ -432,11 +421,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
                         err |= DEV_OVERFLOW;
                         D = make_fn(&S.leaf31, 1, leaf31_sl, 1);
                     } else {
-                        const volatile int* hp = reinterpret_cast<const volatile int*>(&chdr_i[t + 1]);
+                        const CarryPtrs ci = carry_ptrs(L, wb, tree, s, split, true);
+                        const volatile int* hp = reinterpret_cast<const volatile int*>(&ci.chdr[t + 1]);
                         const int2 h = make_int2(hp[0], hp[1]);
-                        const double csl = *(volatile const double*)&csl_i[t + 1];
-                        D = (h.y < 0) ? make_fn(cv_i + (size_t)(t + 1) * C, h.x, csl, 1)
-                                      : make_fn(ca_i + h.y, h.x, csl, 1);
+                        const double csl = *(volatile const double*)&ci.csl[t + 1];
+                        D = (h.y < 0) ? make_fn(ci.cv + (size_t)(t + 1) * C, h.x, csl, 1)
+                                      : make_fn(ci.ca + h.y, h.x, csl, 1);
                     }
                 } else {
                     D = make_fn(&S.leaf31, 0, 0.0, 1);
@@ -558,21 +548,22 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
                 {
                     const int c_n = __shfl_sync(FULL, my_n, 0);
                     const int c_off = __shfl_sync(FULL, my_off, 0);
-                    if (lane == 0) csl_o[t] = my_sl;
+                    const CarryPtrs co = carry_ptrs(L, wb, tree, s, split, false);
+                    if (lane == 0) co.csl[t] = my_sl;
                     if (c_off < 0) {
-                        if (lane < c_n) cv_o[(size_t)t * C + lane] = S.row[lane * SW];
-                        if (lane == 0) chdr_o[t] = make_int2(c_n, -1);
+                        if (lane < c_n) co.cv[(size_t)t * C + lane] = S.row[lane * SW];
+                        if (lane == 0) co.chdr[t] = make_int2(c_n, -1);
                     } else {
                         int base = 0;
-                        if (lane == 0) base = atomicAdd(ccnt, c_n);
+                        if (lane == 0) base = atomicAdd(split ? &L.carena_cnt[tree] : &S.ccnt, c_n);
                         base = __shfl_sync(FULL, base, 0);
-                        if (base + c_n > ccap) {
+                        if (base + c_n > (split ? L.carena_split_cap : L.caps.carena_cap)) {
                             err |= DEV_OVERFLOW;
                         } else {
-                            Vtx* const ca = ca_o + base;
+                            Vtx* const ca = co.ca + base;
                             const Vtx* const ra = WS(Vtx, rarena, nxt) + c_off;
                             for (int i = lane; i < c_n; i += 32) ca[i] = ra[i];
-                            if (lane == 0) chdr_o[t] = make_int2(c_n, base);
+                            if (lane == 0) co.chdr[t] = make_int2(c_n, base);
                         }
                     }
                     if (prog_out) {  // split mode: publish level t to strip s-1
@@ -633,6 +624,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
         }
     }
 }
+
+#undef Epow
+#undef Dpow
+#undef hscr
+#undef zbuf
 
 // ---------------------------------------------------------------------------
 // host side
