@@ -39,20 +39,14 @@ __device__ __forceinline__ double min_nonneg(double a, double b) {
 }
 constexpr int CRR_THREADS = 128;
 
-template <int C, int KIND>
-__device__ __forceinline__ double crr_tree(int lane, int N, double S0, double K, double K2, double h, double rho,
-                                           bool euro) {
+template <int C, int KIND, bool EURO>
+__device__ __forceinline__ double crr_tree(int lane, int N, double S0, double K, double K2, double h, double rho) {
     const double u = exp(h), d = 1.0 / u, r = exp(rho);
     const double p = (r - d) / (u - d);
     const double pu = p / r, pd = (1.0 - p) / r;
     const double c0 = (KIND == KIND_PUT) ? K * (1.0 - d) : -K * (1.0 - d);
-    // along a lane's block, S_{t,j+1} = d^2 S_{t,j}: X_{q+1} = d^2 X_q + c2
-    const double d2 = d * d;
-    const double c2 = (KIND == KIND_PUT) ? K * (1.0 - d2) : -K * (1.0 - d2);
 
-    // only the first node's exercise state of each slot is carried (registers:
-    // C instead of C x M), the others are rebuilt along the block every level
-    double V[C][CRR_M], Xb[C];
+    double V[C][CRR_M], X[C][CRR_M];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
 #pragma unroll
@@ -63,7 +57,7 @@ __device__ __forceinline__ double crr_tree(int lane, int N, double S0, double K,
             if (KIND == KIND_PUT) x = K - S;
             else if (KIND == KIND_CALL) x = S - K;
             else x = S;  // bull: X holds S
-            if (q == 0) Xb[c] = x;
+            X[c][q] = x;
             V[c][q] = (KIND == KIND_BULL) ? fmin(fmax(S - K, 0.0), K2 - K) : fmax(x, 0.0);
         }
     }
@@ -73,22 +67,19 @@ __device__ __forceinline__ double crr_tree(int lane, int N, double S0, double K,
             if (32 * c * CRR_M > t) break;  // warp-uniform: slot c holds no live node
             const double send = (lane == 0) ? ((c + 1 < C) ? V[c + 1][0] : 0.0) : V[c][0];
             const double nb = __shfl_sync(0xffffffffu, send, (lane + 1) & 31);
-            double x;
-            if (KIND == KIND_BULL) x = (Xb[c] *= d);
-            else x = Xb[c] = fma(d, Xb[c], c0);
 #pragma unroll
             for (int q = 0; q < CRR_M; ++q) {
                 const double vn = (q + 1 < CRR_M) ? V[c][q + 1] : nb;
                 double ex;
                 if (KIND == KIND_BULL) {
-                    ex = min_nonneg(max_nonneg(x - K, 0.0), K2 - K);
-                    x *= d2;
+                    X[c][q] *= d;
+                    ex = min_nonneg(max_nonneg(X[c][q] - K, 0.0), K2 - K);
                 } else {
-                    ex = x;
-                    x = fma(d2, x, c2);
+                    X[c][q] = fma(d, X[c][q], c0);
+                    ex = X[c][q];
                 }
                 const double cont = fma(pu, V[c][q], pd * vn);
-                V[c][q] = euro ? cont : max_nonneg(ex, cont);  // European: no early exercise (NEXT #3)
+                V[c][q] = EURO ? cont : max_nonneg(ex, cont);  // European: no early exercise (NEXT #3)
             }
         }
     }
@@ -116,9 +107,15 @@ __global__ void __launch_bounds__(CRR_THREADS, AMTC_CRR_MINB) crr_kernel(BatchPt
     ok = ok && (rho < h) && (-h < rho);  // d < r < u
     double v = NAN;
     if (ok) {  // warp-uniform
-        if (kind == KIND_PUT) v = crr_tree<C, KIND_PUT>(lane, N, S0, K, K2, h, rho, euro);
-        else if (kind == KIND_CALL) v = crr_tree<C, KIND_CALL>(lane, N, S0, K, K2, h, rho, euro);
-        else v = crr_tree<C, KIND_BULL>(lane, N, S0, K, K2, h, rho, euro);
+        if (euro) {
+            if (kind == KIND_PUT) v = crr_tree<C, KIND_PUT, true>(lane, N, S0, K, K2, h, rho);
+            else if (kind == KIND_CALL) v = crr_tree<C, KIND_CALL, true>(lane, N, S0, K, K2, h, rho);
+            else v = crr_tree<C, KIND_BULL, true>(lane, N, S0, K, K2, h, rho);
+        } else {
+            if (kind == KIND_PUT) v = crr_tree<C, KIND_PUT, false>(lane, N, S0, K, K2, h, rho);
+            else if (kind == KIND_CALL) v = crr_tree<C, KIND_CALL, false>(lane, N, S0, K, K2, h, rho);
+            else v = crr_tree<C, KIND_BULL, false>(lane, N, S0, K, K2, h, rho);
+        }
     }
     if (lane == 0) out[w] = v;
 }
