@@ -82,7 +82,7 @@ __global__ void tree_leaves_kernel(TreeConsts c, int N, int64_t j0, int64_t n, d
 
 // one band: levels t_top-1 .. t_top-D'; vin holds level t_top for columns
 // [jin0, jin0 + nin); vout receives level t_top - D' for [jout0, jout0 + nout)
-template <int KIND>
+template <int KIND, bool EURO>
 __global__ void __launch_bounds__(TREE_THREADS) tree_band_kernel(TreeConsts c, int t_top, int Dp,
                                                                  const double* __restrict__ vin, int64_t jin0,
                                                                  int64_t nin, double* __restrict__ vout,
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(TREE_THREADS) tree_band_kernel(TreeConsts c, i
                 ex = X[q];
             }
             const double cont = fma(c.pu, V[q], c.pd * vn);
-            V[q] = c.euro ? cont : max_nonneg(ex, cont);
+            V[q] = EURO ? cont : max_nonneg(ex, cont);
         }
     }
 #pragma unroll
@@ -162,12 +162,17 @@ static void launch_band(const TreeConsts& c, int t_top, int Dp, const double* vi
     if (nout <= 0) return;
     const int64_t warps = (nout + TREE_W - 1) / TREE_W;
     const unsigned blocks = (unsigned)((warps * 32 + TREE_THREADS - 1) / TREE_THREADS);
-    if (c.kind == KIND_PUT)
-        tree_band_kernel<KIND_PUT><<<blocks, TREE_THREADS, 0, s>>>(c, t_top, Dp, vin, jin0, nin, vout, jout0, nout);
-    else if (c.kind == KIND_CALL)
-        tree_band_kernel<KIND_CALL><<<blocks, TREE_THREADS, 0, s>>>(c, t_top, Dp, vin, jin0, nin, vout, jout0, nout);
-    else
-        tree_band_kernel<KIND_BULL><<<blocks, TREE_THREADS, 0, s>>>(c, t_top, Dp, vin, jin0, nin, vout, jout0, nout);
+#define AMTC_BAND(K, E) tree_band_kernel<K, E><<<blocks, TREE_THREADS, 0, s>>>(c, t_top, Dp, vin, jin0, nin, vout, jout0, nout)
+    if (c.euro) {
+        if (c.kind == KIND_PUT) AMTC_BAND(KIND_PUT, true);
+        else if (c.kind == KIND_CALL) AMTC_BAND(KIND_CALL, true);
+        else AMTC_BAND(KIND_BULL, true);
+    } else {
+        if (c.kind == KIND_PUT) AMTC_BAND(KIND_PUT, false);
+        else if (c.kind == KIND_CALL) AMTC_BAND(KIND_CALL, false);
+        else AMTC_BAND(KIND_BULL, false);
+    }
+#undef AMTC_BAND
     note_launch();
 }
 
