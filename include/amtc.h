@@ -141,7 +141,7 @@ int amtc_price_crr_batch_host(const amtc_batch_soa* h_in, int64_t n, int32_t N, 
 
 /*
  * k = 0 CRR price of ONE large tree on the current device (config 5a, N up to
- * 10^5 and beyond).  The level is swept in bands of 128
+ * 10^5 and beyond).  The level is swept in bands of 256
  * levels over warp tiles with ghost columns (region-B dependency).
  * Synchronous on cuda_stream.  *price (HOST pointer) receives V_0(0); NaN and a
  * non-zero status on invalid input (as amtc_price_crr_batch's validation).
@@ -164,7 +164,7 @@ int amtc_comm_destroy(void* comm);
  * (SURVEY 8(e), config 5): every rank calls it with the same arguments.  k = 0:
  * rank g owns columns [ceil(g w/na), ceil((g+1) w/na)) of the current level
  * (w = t+1) on the first na = clamp(w/4096, 1, nranks) ranks,
- * re-split every band of 128 levels (the paper's per-round rebalancing,
+ * re-split every band of 256 levels (the paper's per-round rebalancing,
  * P:178); before each band the ranks exchange their window halos with
  * ncclSend/ncclRecv (region-B dependency).  k > 0: the tree's
  * 32-column strips (strip-split mode of the transaction-cost solver) are

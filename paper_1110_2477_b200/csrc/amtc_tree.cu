@@ -8,11 +8,11 @@
 // D levels over output columns [j0, j0 + W) is the input window [j0, j0 + W + D)
 // at the band's top level (the paper's region-B dependency).
 //
-// Band kernel: each warp owns M = 16 consecutive columns per lane (512 columns,
-// the level in registers); it reads the 512-column window at level t_top,
-// runs D = 128 levels with one 64-bit shuffle per level (the j+1 neighbour of
-// a lane's last column), and writes the first 384 columns of level t_top - D
-// (the right 128 columns become invalid one per level: the ghost zone).  A
+// Band kernel: each warp owns M = 16 (or 24) consecutive columns per lane (32 M
+// columns, the level in registers); it reads its window at level t_top, runs
+// D = 256 levels with one 64-bit shuffle per level (the j+1 neighbour of a
+// lane's last column), and writes the first 32 M - D columns of level t_top - D
+// (the right D columns become invalid one per level: the ghost zone).  A
 // band is one launch; the level lives in HBM/L2 between bands (800 KB at
 // N = 10^5).  No shared memory, no __syncthreads: warps are independent.
 //
@@ -45,10 +45,11 @@
 
 namespace amtc {
 
-constexpr int TREE_M = 16;                      // columns per lane
-constexpr int TREE_COLS = 32 * TREE_M;          // window columns per warp
-constexpr int TREE_D = 128;                     // levels per band
-constexpr int TREE_W = TREE_COLS - TREE_D;      // output columns per warp
+// band shapes (measured on B200): 16 columns per lane and 256 levels per band
+// for N <= 3e5 (N = 1e5: 17.4 ms vs 21.8 ms at 128 levels), 24 columns per lane
+// and 256 levels beyond (N = 1e6: 360 ms vs 375 ms); the right D columns of a
+// warp's window are its ghost zone
+constexpr int TREE_D = 256;  // levels per band (both shapes)
 constexpr int TREE_THREADS = 128;
 
 struct TreeConsts {
@@ -82,11 +83,12 @@ __global__ void tree_leaves_kernel(TreeConsts c, int N, int64_t j0, int64_t n, d
 
 // one band: levels t_top-1 .. t_top-D'; vin holds level t_top for columns
 // [jin0, jin0 + nin); vout receives level t_top - D' for [jout0, jout0 + nout)
-template <int KIND, bool EURO>
+template <int TREE_M, int KIND, bool EURO>
 __global__ void __launch_bounds__(TREE_THREADS) tree_band_kernel(TreeConsts c, int t_top, int Dp,
                                                                  const double* __restrict__ vin, int64_t jin0,
                                                                  int64_t nin, double* __restrict__ vout,
                                                                  int64_t jout0, int64_t nout) {
+    constexpr int TREE_W = 32 * TREE_M - TREE_D;  // output columns per warp
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t jw = jout0 + w * TREE_W;
@@ -157,12 +159,14 @@ static void launch_leaves(const TreeConsts& c, int N, int64_t j0, int64_t n, dou
     note_launch();
 }
 
-static void launch_band(const TreeConsts& c, int t_top, int Dp, const double* vin, int64_t jin0, int64_t nin,
-                        double* vout, int64_t jout0, int64_t nout, cudaStream_t s) {
-    if (nout <= 0) return;
-    const int64_t warps = (nout + TREE_W - 1) / TREE_W;
+template <int M>
+static void launch_band_m(const TreeConsts& c, int t_top, int Dp, const double* vin, int64_t jin0, int64_t nin,
+                          double* vout, int64_t jout0, int64_t nout, cudaStream_t s) {
+    constexpr int W = 32 * M - TREE_D;
+    const int64_t warps = (nout + W - 1) / W;
     const unsigned blocks = (unsigned)((warps * 32 + TREE_THREADS - 1) / TREE_THREADS);
-#define AMTC_BAND(K, E) tree_band_kernel<K, E><<<blocks, TREE_THREADS, 0, s>>>(c, t_top, Dp, vin, jin0, nin, vout, jout0, nout)
+#define AMTC_BAND(K, E) \
+    tree_band_kernel<M, K, E><<<blocks, TREE_THREADS, 0, s>>>(c, t_top, Dp, vin, jin0, nin, vout, jout0, nout)
     if (c.euro) {
         if (c.kind == KIND_PUT) AMTC_BAND(KIND_PUT, true);
         else if (c.kind == KIND_CALL) AMTC_BAND(KIND_CALL, true);
@@ -173,6 +177,13 @@ static void launch_band(const TreeConsts& c, int t_top, int Dp, const double* vi
         else AMTC_BAND(KIND_BULL, false);
     }
 #undef AMTC_BAND
+}
+
+static void launch_band(const TreeConsts& c, int N, int t_top, int Dp, const double* vin, int64_t jin0, int64_t nin,
+                        double* vout, int64_t jout0, int64_t nout, cudaStream_t s) {
+    if (nout <= 0) return;
+    if (N <= 300000) launch_band_m<16>(c, t_top, Dp, vin, jin0, nin, vout, jout0, nout, s);
+    else launch_band_m<24>(c, t_top, Dp, vin, jin0, nin, vout, jout0, nout, s);
     note_launch();
 }
 
@@ -291,7 +302,7 @@ static int tree_run(const TreeConsts& c, int N, ncclComm_t comm, int rank, int n
             }
         }
         const int64_t a0 = split_at(w0, rank, nranks), b0 = split_at(w0, rank + 1, nranks);
-        launch_band(c, t_top, Dp, win, my_lo, my_hi - my_lo, nxt, a0, b0 - a0, s);
+        launch_band(c, N, t_top, Dp, win, my_lo, my_hi - my_lo, nxt, a0, b0 - a0, s);
         std::swap(cur, nxt);
         a = a0;
         b = b0;
