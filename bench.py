@@ -296,6 +296,13 @@ def run_amtc(args):
                                else "6 flop per CRR node-update (DESIGN.md)")}
     if args.config == 4:
         roofline["vertex_sum_per_step"] = vertex_sum / args.steps
+        tf = os.path.join(ROOT, "profiles", "r01_traffic_config4.json")
+        if os.path.exists(tf):
+            try:
+                roofline["traffic"] = float(json.load(open(tf))["traffic_bytes_per_step"])
+                roofline["traffic_source"] = "ncu dram__bytes_read+write of one step (profiles/r01_traffic_config4.json)"
+            except Exception:
+                pass
 
     # end to end through the public C-ABI with HOST buffers (pinned), H2D + D2H inside
     e2e = None

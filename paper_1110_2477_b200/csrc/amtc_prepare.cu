@@ -19,8 +19,11 @@ constexpr int N_CLASSES = TC_CLASSES;
 // cost class of an item: the buyer of a call / bull spread grows "teeth" when
 // k/h is large (breakpoint counts measured with the oracle), so
 // those items are scheduled first (longest-processing-time order)
+// Class 0 (the light kernel): put buyers and sellers of puts / calls; the bull
+// spread's seller grows heavy functions too (measured: 230 config-4 bull sellers
+// overflowed the light kernel), so both bull items take the full kernel.
 __device__ __forceinline__ int item_class(const OptionConsts& oc, int party) {
-    if (party == 0 || oc.kind == KIND_PUT) return 0;
+    if (oc.kind == KIND_PUT || (party == 0 && oc.kind == KIND_CALL)) return 0;
     double kh = oc.k / oc.h;
     return min(N_CLASSES - 1, 1 + (int)(4.0 * kh));
 }
