@@ -305,15 +305,18 @@ struct Stage {
 // Stage z's vertices strictly inside (a, b); a finite or -inf (then the state
 // at -inf is given: v = the M line, u = its lo line, zU0 = u wins there).
 // s_cur: z's slope just right of a.  Returns z's slope just left of b.
+// vi0 >= 0: z's state just right of a is already known (vi0, zU0: z_side's
+// outputs at a), otherwise it is evaluated here.
 template <class Out>
 __device__ __forceinline__ double emit_open(double a, double b, const Line& LW, const Line& LM, bool hasM,
                                             const Line& LP, bool hasP, const PCtx& c, double s_cur, bool zU0,
-                                            Out& st) {
+                                            Out& st, int vi0 = -1) {
     double pos = a;
     int vi;
     bool zU;
     double zv;
-    if (isfinite(a)) z_side(LW, LM, hasM, LP, hasP, c, a, true, vi, zU, zv);
+    if (vi0 >= 0) { vi = vi0; zU = zU0; }
+    else if (isfinite(a)) z_side(LW, LM, hasM, LP, hasP, c, a, true, vi, zU, zv);
     else { vi = hasM ? 1 : 0; zU = zU0; }
     // events closer than xtol() to either end are rounding images of the end
     // vertex itself (e.g. the M line passes through the vertex that defines it)
@@ -349,6 +352,52 @@ __device__ __forceinline__ double emit_open(double a, double b, const Line& LW, 
     }
     return s_cur;
 }
+
+// z = W on the whole piece [x, xn) of the W vertex (x, f, s) (the common case
+// inside the buyer's sawtooth): v = W there -- the piece's slope lies in
+// [lo, hi], the M line (slope lo <= s) starts above W by more than ftol (or
+// within ftol when parallel to the piece) and does not dip below W before xn, the P line (slope hi >= s) starts at or above
+// W within ftol -- and u loses to v by more than ftol at the piece's ends and
+// at u's kink inside it.  Then the piece emits just its vertex (x, f, s),
+// which is what z_side + emit_open produce in that case, without their
+// per-line crossing searches.
+__device__ __forceinline__ bool piece_is_w(double x, double f, double s, double xn, double Mnext, double Pj,
+                                           const PCtx& c) {
+    if (!(s >= c.lo && s <= c.hi)) return false;
+    const double p = fma(c.hi, x, Pj);
+    if (p < f - ftol(p, f)) return false;
+    const bool fin = isfinite(xn);
+    const double wn = fin ? fma(s, xn - x, f) : 0.0;
+    if (isfinite(Mnext)) {
+        if (!fin) return false;
+        const double m = fma(c.lo, x, Mnext);
+        const double tm = ftol(m, f);
+        // a tie at x keeps W only when the M line is parallel to the piece (z_side's slope rule)
+        if (!(m > f + tm || (s == c.lo && m >= f - tm))) return false;
+        const double mn = fma(c.lo, xn, Mnext);
+        if (mn < wn - ftol(mn, wn)) return false;
+    }
+    const double u0 = fma(x >= c.ux ? c.hi : c.lo, x - c.ux, c.uf);
+    if (c.seller) {
+        if (!fin || !(f > u0 + ftol(u0, f))) return false;
+        const double un = fma(xn > c.ux ? c.hi : c.lo, xn - c.ux, c.uf);
+        return wn > un + ftol(un, wn);
+    }
+    if (!(u0 > f + ftol(u0, f))) return false;
+    if (fin) {
+        const double un = fma(xn > c.ux ? c.hi : c.lo, xn - c.ux, c.uf);
+        if (!(un > wn + ftol(un, wn))) return false;
+    }
+    if (x < c.ux && c.ux < xn) {
+        const double wk = fma(s, c.ux - x, f);
+        if (!(c.uf > wk + ftol(c.uf, wk))) return false;
+    }
+    return true;
+}
+
+#ifndef AMTC_HEAVY_STAT
+#define AMTC_HEAVY_STAT(i)
+#endif
 
 // warp-level scans
 __device__ __forceinline__ double warp_min(double v) {
@@ -1114,7 +1163,17 @@ __device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo,
         st.last_s = NAN;
         double s_run = NAN;
         bool pending = false;
-        if (has) {
+        const double Pj = fmin(Pl, hl);
+        const bool fast = has && !first_overall && piece_is_w(wv.x, wv.f, wv.s, xn, Mnext, Pj, c);
+        AMTC_HEAVY_STAT(has ? (fast ? 1 : 2) : 0);
+#ifdef AMTC_HEAVY_STAT_BLOCKS
+        if (__ballot_sync(FULLM, has && !fast) == 0u && lane == 0) AMTC_HEAVY_STAT(3);
+#endif
+        if (fast) {
+            pending = true;
+            st.push(wv.x, wv.f, wv.s);
+            s_run = wv.s;
+        } else if (has) {
             const double Mj = fmin(gl, Mnext);
             if (first_overall) {
                 const Line LW{wv.x, wv.f, sL}, LM{0.0, Mj, lo}, LP{0.0, INFINITY, hi};
@@ -1126,7 +1185,6 @@ __device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo,
             int vi;
             bool zU;
             double zv;
-            const double Pj = fmin(Pl, hl);
             const Line LWr{wv.x, wv.f, wv.s}, LMr{0.0, Mnext, lo}, LPr{0.0, Pj, hi};
             const double sr_ = z_side(LWr, LMr, isfinite(Mnext), LPr, true, c, wv.x, true, vi, zU, zv);
             if (s_run != s_run) {
@@ -1135,7 +1193,7 @@ __device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo,
             } else if (sr_ != s_run) {
                 st.push(wv.x, zv, sr_);
             }
-            s_run = emit_open(wv.x, xn, LWr, LMr, isfinite(Mnext), LPr, true, c, sr_, false, st);
+            s_run = emit_open(wv.x, xn, LWr, LMr, isfinite(Mnext), LPr, true, c, sr_, zU, st, vi);
         }
         const double s_end = s_run;
         // the slope arriving from the left: s_end of the previous lane (all lanes

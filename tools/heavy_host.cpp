@@ -4,6 +4,14 @@
 // stdin: "S0 K K2 T sigma R k kind N" per line; stdout per line:
 //   "<nodes> <max vertex excess> <max rel value diff> <status>"
 #include "warp_emu.h"
+#include <atomic>
+// sweep-C piece statistics (0 empty lane, 1 fast piece, 2 general piece, 3 all-fast block)
+static std::atomic<long> g_stat[4];
+static bool g_count = false;
+#define AMTC_HEAVY_STAT(i) (g_count ? (void)g_stat[(i)].fetch_add(1, std::memory_order_relaxed) : (void)0)
+#define AMTC_HEAVY_STAT_BLOCKS 1
+static std::atomic<long> g_why[32];
+#define AMTC_WHY(i) (g_count ? (void)g_why[(i)].fetch_add(1) : (void)0)
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
@@ -69,6 +77,7 @@ int main(int argc, char** argv) {
                         arena(8 * (U.n + D.n) + 64);
                     int counter = 0, zoff = 0, nZ = 0, err = 0;
                     heavy::HWin win;
+                    g_count = U.n + D.n > 64;
                     warp_emu::run_warp([&](int lane) {
                         int zo, zn;
                         const int e = block_variant
@@ -107,6 +116,9 @@ int main(int argc, char** argv) {
             }
         }
         std::printf("%ld %d %.3g %d\n", nodes, worst_excess, worst_rel, status);
+        std::fprintf(stderr, "pieces: fast %ld general %ld empty-lane %ld all-fast blocks %ld\n", g_stat[1].load(),
+                     g_stat[2].load(), g_stat[0].load(), g_stat[3].load());
+        for (int i = 0; i < 32; ++i) if (g_why[i]) std::fprintf(stderr, " why %d: %ld\n", i, g_why[i].load());
         std::fflush(stdout);
     }
     return 0;
