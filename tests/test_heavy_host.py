@@ -47,7 +47,14 @@ def test_heavy_matches_lane_forced(heavy_host, tl):
 
 
 def test_heavy_matches_lane_sawtooth(heavy_host):
-    """A call at large k/h (the buyer's sawtooth grows to ~40 vertices at N = 80)."""
+    """A call at large k/h (the buyer's sawtooth grows to ~40 vertices at N = 80).
+    Nodes above 16 child vertices feed the warp path's result forward; both
+    branches of sweep C (the z = W fast path and the general emission) must
+    occur on the sawtooth (the harness counts them on stderr)."""
     line = "100.0 106.5 0.0 0.6 0.3 0.018 0.017 1 80"
-    for nodes, excess, rel, st in run(heavy_host, [line], 64):
+    p = subprocess.run([heavy_host, "16"], input=line + "\n", capture_output=True, text=True, check=True, timeout=600)
+    for nodes, excess, rel, st in (ln.split() for ln in p.stdout.strip().splitlines()):
         assert st == "0" and int(excess) <= 1 and float(rel) < 1e-11
+    stats = p.stderr.split()
+    fast, general = int(stats[stats.index("fast") + 1]), int(stats[stats.index("general") + 1])
+    assert fast > 0 and general > 0

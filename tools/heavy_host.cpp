@@ -77,7 +77,7 @@ int main(int argc, char** argv) {
                         arena(8 * (U.n + D.n) + 64);
                     int counter = 0, zoff = 0, nZ = 0, err = 0;
                     heavy::HWin win;
-                    g_count = U.n + D.n > 64;
+                    g_count = U.n + D.n > (tl > 0 ? tl : 64);
                     warp_emu::run_warp([&](int lane) {
                         int zo, zn;
                         const int e = block_variant
