@@ -219,6 +219,27 @@ __device__ __forceinline__ Fn shfl_fn(const Fn& F, int src) {
 // serve until the CTA is idle.  A claimed node is updated by the whole warp
 // (pwl_heavy.cuh) into the claimer's scratch and copied into the owner's row
 // arena.  Returns true if a node was served.
+
+// warp copy of n vertices between global buffers that never overlap, as 3n
+// doubles with eight loads in flight per lane before the stores (the compiler
+// cannot reorder a load above a store through possibly aliasing pointers, so a
+// plain loop waits one memory latency per 32 vertices)
+static_assert(sizeof(Vtx) == 3 * sizeof(double), "warp_copy_vtx copies vertices as doubles");
+__device__ __forceinline__ void warp_copy_vtx(Vtx* dst, const Vtx* src, int n, int lane) {
+    const double* __restrict__ sp = reinterpret_cast<const double*>(src);
+    double* __restrict__ dp = reinterpret_cast<double*>(dst);
+    const int m = 3 * n;
+    int i = lane;
+    for (; i + 224 < m; i += 256) {
+        double r[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) r[q] = sp[i + 32 * q];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dp[i + 32 * q] = r[q];
+    }
+    for (; i < m; i += 32) dp[i] = sp[i];
+}
+
 template <int C, int B, int WARPS>
 __device__ __noinline__ bool serve_one(CtaHdr& H, StripSmem<C, B, true>* all, int me, Vtx* hscr, int hcap, Vtx* zbuf,
                                        int zcap, int lane) {
@@ -269,7 +290,7 @@ __device__ __noinline__ bool serve_one(CtaHdr& H, StripSmem<C, B, true>* all, in
         off = __shfl_sync(FULL, off, 0);
         if (off + nZ > O.h_acap) e = DEV_OVERFLOW;
         else
-            for (int i = lane; i < nZ; i += 32) O.h_arena[off + i] = zbuf[i];
+            warp_copy_vtx(O.h_arena + off, zbuf, nZ, lane);
     }
     __syncwarp();
     if (lane == 0) {
@@ -562,7 +583,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
                         } else {
                             Vtx* const ca = co.ca + base;
                             const Vtx* const ra = WS(Vtx, rarena, nxt) + c_off;
-                            for (int i = lane; i < c_n; i += 32) ca[i] = ra[i];
+                            warp_copy_vtx(ca, ra, c_n, lane);
                             if (lane == 0) co.chdr[t] = make_int2(c_n, base);
                         }
                     }
