@@ -55,7 +55,9 @@ class _Quote(C.Structure):
     _fields_ = [("ask", C.c_double), ("bid", C.c_double), ("status", C.c_int32),
                 ("max_kinks_ask", C.c_int32), ("max_kinks_bid", C.c_int32), ("pad", C.c_int32),
                 ("sum_kinks_ask", C.c_int64), ("sum_kinks_bid", C.c_int64),
-                ("crossings", C.c_int64), ("hedge_ask", C.c_double), ("hedge_bid", C.c_double)]
+                ("crossings", C.c_int64), ("hedge_ask", C.c_double), ("hedge_bid", C.c_double),
+                ("fp64_ops", C.c_int64), ("merge_visits", C.c_int64), ("restrict_cvx", C.c_int64),
+                ("restrict_ncvx", C.c_int64), ("scale_visits", C.c_int64)]
 
 
 _lib = None
@@ -68,6 +70,9 @@ def lib():
         dp = C.POINTER(C.c_double)
         ip = C.POINTER(C.c_int)
         _lib.oracle_price_tc.argtypes = [C.POINTER(_Option), C.c_int, C.POINTER(_Quote), C.POINTER(C.c_int32)]
+        _lib.oracle_price_tc_stats.argtypes = [C.POINTER(_Option), C.c_int, C.POINTER(_Quote),
+                                               C.POINTER(C.c_int32), C.POINTER(C.c_int64)]
+        _lib.oracle_kink_bin_hi.argtypes = [C.c_int]
         _lib.oracle_price_crr.argtypes = [C.POINTER(_Option), C.c_int, dp]
         _lib.oracle_price_euro_closed.argtypes = [C.POINTER(_Option), C.c_int, dp]
         _lib.oracle_pwl_op.argtypes = [C.c_int, C.c_int, dp, dp, C.c_double, C.c_double,
@@ -112,21 +117,56 @@ class Quote:
     crossings: int
     hedge_ask: float = float("nan")
     hedge_bid: float = float("nan")
+    # SURVEY 8(d) cost model, counted by the oracle (instrumentation only):
+    # fp64_ops = 3 merge_visits + 4 crossings + 2 restrict_cvx + 4 restrict_ncvx
+    #            + 2 scale_visits over every node t <= N, both parties
+    fp64_ops: int = 0
+    merge_visits: int = 0
+    restrict_cvx: int = 0
+    restrict_ncvx: int = 0
+    scale_visits: int = 0
 
 
-def price_tc(opt: Option, N: int, kinks: bool = False):
+def _quote(q) -> "Quote":
+    return Quote(q.ask, q.bid, q.status, q.max_kinks_ask, q.max_kinks_bid, q.sum_kinks_ask,
+                 q.sum_kinks_bid, q.crossings, q.hedge_ask, q.hedge_bid, q.fp64_ops,
+                 q.merge_visits, q.restrict_cvx, q.restrict_ncvx, q.scale_visits)
+
+
+def lvl_stride() -> int:
+    return lib().oracle_lvl_stride()
+
+
+def new_level_stats(N: int) -> np.ndarray:
+    """Accumulator for price_tc(..., level_stats=acc): int64 array of shape
+    (2, N+1, stride); [p, t, 0] = max kinks on level t, [p, t, 1] = sum of kinks,
+    [p, t, 2+b] = number of nodes in kink bin b (kink_bin_hi(b) = bin's top)."""
+    return np.zeros((2, N + 1, lvl_stride()), dtype=np.int64)
+
+
+def kink_bin_hi(b: int) -> int:
+    return lib().oracle_kink_bin_hi(int(b))
+
+
+def price_tc(opt: Option, N: int, kinks: bool = False, level_stats: np.ndarray | None = None):
     """Ask/bid under proportional costs (Sec. 3 + 4.1).  With kinks=True also
-    returns the per-node kink counts, shape (N+1)(N+2)/2 x 2 (seller, buyer)."""
+    returns the per-node kink counts, shape (N+1)(N+2)/2 x 2 (seller, buyer).
+    level_stats (optional, from new_level_stats(N)) accumulates the per-level
+    kink max / sum / histogram of this option into the caller's array."""
     q = _Quote()
     arr = None
     ptr = None
     if kinks:
         arr = np.zeros(((N + 1) * (N + 2) // 2, 2), dtype=np.int32)
         ptr = arr.ctypes.data_as(C.POINTER(C.c_int32))
+    lptr = None
+    if level_stats is not None:
+        assert level_stats.dtype == np.int64 and level_stats.shape == (2, N + 1, lvl_stride())
+        assert level_stats.flags.c_contiguous
+        lptr = level_stats.ctypes.data_as(C.POINTER(C.c_int64))
     o = opt._c()
-    lib().oracle_price_tc(C.byref(o), N, C.byref(q), ptr)
-    out = Quote(q.ask, q.bid, q.status, q.max_kinks_ask, q.max_kinks_bid, q.sum_kinks_ask,
-                q.sum_kinks_bid, q.crossings, q.hedge_ask, q.hedge_bid)
+    lib().oracle_price_tc_stats(C.byref(o), N, C.byref(q), ptr, lptr)
+    out = _quote(q)
     return (out, arr) if kinks else out
 
 

@@ -70,10 +70,31 @@ typedef struct {
     double sr; /* slope on (x[n-1], +inf) */
 } pwl;
 
-/* operation counters (instrumentation only; not part of any result) */
+/*
+ * Operation counters (instrumentation only; never part of any result).
+ * The SURVEY 8(d) cost model of "algorithmic FP64 ops" is applied to them in
+ * oracle_price_tc_stats():
+ *   merge visit (one candidate abscissa of max/min: evaluate the other
+ *                function there and compare)                      = 3
+ *   crossing    (2 DADD + 1 DDIV + 1 DFMA)                           = 4
+ *   restriction visit (one vertex of f = w/r in one scan pass):
+ *                2 when f is convex (clip compares), 4 when not      = 2 | 4
+ *   scaling by 1/r, per vertex of w                                  = 2
+ *   max/min with the expense function u                              = as merge
+ * The counts follow the DEFINITION of each step (union of both vertex sets
+ * for an envelope, one visit per vertex per scan pass), not the oracle's
+ * allocation pattern; the min(A, B) that closes the restriction is part of
+ * the restriction's definition (its candidates are not merge visits; its
+ * crossings are crossings).
+ */
 typedef struct {
-    int64_t vertices_out; /* sum of output vertex counts of every z */
-    int64_t crossings;    /* crossing points solved (one division each) */
+    int64_t vertices_out;    /* sum of output vertex counts of every z */
+    int64_t crossings;       /* crossing points solved (one division each) */
+    int64_t merge_visits;    /* candidate abscissae of max(z^u,z^d) and of max/min(u,v) */
+    int64_t restrict_cvx;    /* restriction scan steps on a convex f */
+    int64_t restrict_ncvx;   /* restriction scan steps on a non-convex f */
+    int64_t scale_visits;    /* vertices of w scaled by 1/r */
+    int in_restrict;         /* set while min(A,B) of a restriction runs */
 } counters;
 
 static int pwl_init(pwl *p, int cap)
@@ -232,6 +253,7 @@ static int pwl_envelope(const pwl *f, const pwl *g, int want_max, pwl *out, coun
         }
     }
     if (pwl_init(out, 2 * nc + 2) != OR_OK) { free(X); return OR_ENOMEM; }
+    if (cnt && !cnt->in_restrict) cnt->merge_visits += nc;
 
     double *D = (double *)calloc((size_t)nc, sizeof(double));
     double *F = (double *)malloc(sizeof(double) * (size_t)nc);
@@ -362,10 +384,26 @@ static int pwl_suffix_inf(const pwl *g, pwl *out, counters *cnt)
  *   B(y) = inf_{y' <= y} [ f(y') - hi*y' ] + hi*y     (sell y-y' shares at -hi)
  * B is computed as the reflection of a suffix infimum.
  */
+/* f is convex iff its slopes (tails included) are non-decreasing */
+static int pwl_is_convex(const pwl *p)
+{
+    double prev = p->sl;
+    for (int i = 0; i + 1 < p->n; i++) {
+        double s = pwl_piece_slope(p, i);
+        if (s < prev) return 0;
+        prev = s;
+    }
+    return p->sr >= prev;
+}
+
 static int pwl_restrict(const pwl *f, double lo, double hi, pwl *out, counters *cnt)
 {
     int st;
     pwl g, G, A, h, hr, Hr, H, B;
+    if (cnt) { /* two scan passes over the vertices of f (cost model above) */
+        if (pwl_is_convex(f)) cnt->restrict_cvx += 2 * (int64_t)f->n;
+        else cnt->restrict_ncvx += 2 * (int64_t)f->n;
+    }
     /* A */
     if ((st = pwl_add_linear(f, -lo, &g)) != OR_OK) return st;
     st = pwl_suffix_inf(&g, &G, cnt);
@@ -388,7 +426,9 @@ static int pwl_restrict(const pwl *f, double lo, double hi, pwl *out, counters *
     st = pwl_add_linear(&H, hi, &B);
     pwl_free(&H);
     if (st != OR_OK) { pwl_free(&A); return st; }
+    if (cnt) cnt->in_restrict = 1;
     st = pwl_envelope(&A, &B, 0, out, cnt);
+    if (cnt) cnt->in_restrict = 0;
     pwl_free(&A);
     pwl_free(&B);
     return st;
@@ -443,7 +483,37 @@ typedef struct {
        w_0 = max(z_{1,0}, z_{1,1}) (no costs at t = 0, so v_0 is the line
        min_y'[w_0(y')/r + S0 y'] - S0 y, derived A.4); smallest minimiser */
     double hedge_ask, hedge_bid;
+    /* SURVEY 8(d) cost model (instrumentation; see "Operation counters"):
+       fp64_ops = 3 merge_visits + 4 crossings + 2 restrict_cvx
+                  + 4 restrict_ncvx + 2 scale_visits, over every node t <= N */
+    int64_t fp64_ops, merge_visits, restrict_cvx, restrict_ncvx, scale_visits;
 } or_quote;
+
+/*
+ * Per-level kink statistics (instrumentation), accumulated (max / +=) into a
+ * caller-owned int64 array of 2 x (N+1) x OR_LVL_STRIDE entries so a caller
+ * can aggregate a batch: entry [party][t][0] = max kinks over the level's
+ * nodes, [1] = sum of kinks, [2 + b] = number of nodes whose kink count falls
+ * in bin b (or_kink_bin: exact below 128, then 8 bins per octave).
+ */
+#define OR_HBINS 240
+#define OR_LVL_STRIDE (2 + OR_HBINS)
+
+static int or_kink_bin(int c)
+{
+    if (c < 128) return c;
+    int e = 0;
+    while ((c >> (e + 1)) != 0) e++; /* e = floor(log2 c) >= 7 */
+    int b = 128 + 8 * (e - 7) + ((c >> (e - 3)) - 8);
+    return b < OR_HBINS ? b : OR_HBINS - 1;
+}
+
+int oracle_kink_bin_hi(int b) /* largest kink count of bin b */
+{
+    if (b < 128) return b;
+    int e = 7 + (b - 128) / 8, sub = (b - 128) % 8;
+    return ((9 + sub) << (e - 3)) - 1;
+}
 
 /* Sec. 4.1: u = exp(sigma sqrt(T/N)), d = 1/u, r = exp(RT/N) */
 static int calibrate(const or_option *o, int N, double *u, double *d, double *r)
@@ -494,6 +564,7 @@ static int node_update_x(int party, const pwl *zu, const pwl *zd, double r, doub
     pwl w, f, v, u;
     if ((st = pwl_envelope(zu, zd, 1, &w, cnt)) != OR_OK) return st; /* w = max(z^u, z^d) */
     st = pwl_div(&w, r, &f);                                        /* w / r */
+    if (cnt) cnt->scale_visits += w.n;
     pwl_free(&w);
     if (st != OR_OK) return st;
     st = pwl_restrict(&f, -Sa, -Sb, &v, cnt);                       /* v */
@@ -519,7 +590,8 @@ static int node_update(int party, const pwl *zu, const pwl *zd, double r, double
  * kinks_out (optional): 2 * (N+1)(N+2)/2 ints, node (t,j) at index
  * 2*(t(t+1)/2 + j) + party, the kink count of z at that node.
  */
-int oracle_price_tc(const or_option *o, int N, or_quote *q, int32_t *kinks_out)
+int oracle_price_tc_stats(const or_option *o, int N, or_quote *q, int32_t *kinks_out,
+                          int64_t *lvl_stats)
 {
     double u, d, r;
     memset(q, 0, sizeof *q);
@@ -527,7 +599,8 @@ int oracle_price_tc(const or_option *o, int N, or_quote *q, int32_t *kinks_out)
     q->hedge_ask = q->hedge_bid = NAN;
     int st = calibrate(o, N, &u, &d, &r);
     if (st != OR_OK) { q->status = st; return st; }
-    counters cnt = {0, 0};
+    counters cnt;
+    memset(&cnt, 0, sizeof cnt);
     pwl *z[2];
     z[0] = (pwl *)calloc((size_t)N + 2, sizeof(pwl));
     z[1] = (pwl *)calloc((size_t)N + 2, sizeof(pwl));
@@ -550,7 +623,7 @@ int oracle_price_tc(const or_option *o, int N, or_quote *q, int32_t *kinks_out)
                 if (t == 0 && !o->cost_t0) {
                     /* root hedge: argmin over the vertices of w_0 of w_0(x)/r + S0 x (A.4) */
                     pwl w;
-                    if ((st = pwl_envelope(&z[party][0], &z[party][1], 1, &w, &cnt)) != OR_OK) break;
+                    if ((st = pwl_envelope(&z[party][0], &z[party][1], 1, &w, NULL)) != OR_OK) break;
                     double best = INFINITY, bx = NAN;
                     for (int i = 0; i < w.n; i++) {
                         double g = w.f[i] / r + S * w.x[i];
@@ -576,6 +649,12 @@ int oracle_price_tc(const or_option *o, int N, or_quote *q, int32_t *kinks_out)
                     if (kk > q->max_kinks_bid) q->max_kinks_bid = kk;
                 }
                 if (kinks_out) kinks_out[2 * ((int64_t)t * (t + 1) / 2 + j) + party] = kk;
+                if (lvl_stats) {
+                    int64_t *L = lvl_stats + ((int64_t)party * (N + 1) + t) * OR_LVL_STRIDE;
+                    if (kk > L[0]) L[0] = kk;
+                    L[1] += kk;
+                    L[2 + or_kink_bin(kk)] += 1;
+                }
             }
         }
     }
@@ -584,12 +663,23 @@ int oracle_price_tc(const or_option *o, int N, or_quote *q, int32_t *kinks_out)
         q->bid = -pwl_eval(&z[1][0], 0.0); /* pi^b_0 = -z'_0(0) */
     }
     q->crossings = cnt.crossings;
+    q->merge_visits = cnt.merge_visits;
+    q->restrict_cvx = cnt.restrict_cvx;
+    q->restrict_ncvx = cnt.restrict_ncvx;
+    q->scale_visits = cnt.scale_visits;
+    q->fp64_ops = 3 * cnt.merge_visits + 4 * cnt.crossings + 2 * cnt.restrict_cvx
+                  + 4 * cnt.restrict_ncvx + 2 * cnt.scale_visits;
     q->status = st;
     for (int p = 0; p < 2; p++) {
         for (int j = 0; j <= N + 1; j++) pwl_free(&z[p][j]);
         free(z[p]);
     }
     return st;
+}
+
+int oracle_price_tc(const or_option *o, int N, or_quote *q, int32_t *kinks_out)
+{
+    return oracle_price_tc_stats(o, N, q, kinks_out, NULL);
 }
 
 /* frictionless exercise value P(S) (P_t = max(K - S_t, 0) for the put) */
@@ -740,4 +830,5 @@ int oracle_node_update(int party, int n1, const double *x1, const double *f1, do
     return st;
 }
 
-int oracle_abi_version(void) { return 1; }
+int oracle_abi_version(void) { return 2; }
+int oracle_lvl_stride(void) { return OR_LVL_STRIDE; }

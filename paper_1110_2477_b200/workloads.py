@@ -48,6 +48,17 @@ class Batch:
                 for f in self.fields()}
 
 
+def soa_sha256(b: Batch) -> str:
+    """SHA-256 of the batch's SoA bytes (fields in Batch.fields() order,
+    little-endian fp64 / int32): the key of the cached oracle reference files."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in Batch.fields():
+        a = getattr(b, f)
+        h.update(np.ascontiguousarray(a, dtype=a.dtype.newbyteorder("<")).tobytes())
+    return h.hexdigest()
+
+
 def concat(batches) -> Batch:
     """Concatenate batches (e.g. the single-tree points of one N)."""
     return Batch(*(np.concatenate([getattr(b, f) for b in batches]) for f in Batch.fields()))

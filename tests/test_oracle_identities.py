@@ -166,3 +166,44 @@ def test_european_below_american_with_costs(kind):
         eu = O.price_tc(O.Option(100.0, 100.0, 1.0, 0.2, 0.05, k, kind, american=False), 60)
         assert eu.ask <= am.ask + 1e-12 and eu.bid <= am.bid + 1e-12
         assert eu.bid <= eu.ask
+
+
+# --- SURVEY 8(c2) step 9 instrumentation: cost-model counters and level stats ---
+
+def test_level_stats_consistent_with_quote():
+    """The per-level kink statistics account for every node t <= N exactly once
+    and agree with the quote's own max / sum of kinks."""
+    N = 60
+    o = O.Option(100.0, 105.0, 0.5, 0.15, 0.05, 0.02, O.CALL)
+    L = O.new_level_stats(N)
+    q = O.price_tc(o, N, level_stats=L)
+    nodes = L[:, :, 2:].sum(axis=2)
+    assert (nodes == np.arange(1, N + 2)[None, :]).all()
+    assert L[0, :, 1].sum() == q.sum_kinks_ask and L[1, :, 1].sum() == q.sum_kinks_bid
+    assert L[0, :, 0].max() == q.max_kinks_ask and L[1, :, 0].max() == q.max_kinks_bid
+    # accumulation: a second call adds the same counts again
+    q2 = O.price_tc(o, N, level_stats=L)
+    assert L[0, :, 1].sum() == 2 * q.sum_kinks_ask and q2.fp64_ops == q.fp64_ops
+
+
+def test_cost_model_counts():
+    """fp64_ops applies the SURVEY 8(d) weights to the counted events; the seller
+    (convex, A.3) never takes a non-convex restriction step, so at k=0 (all
+    functions lines, A.1) every restriction step is convex."""
+    N = 40
+    q = O.price_tc(O.Option(100.0, 100.0, 1.0, 0.2, 0.05, 0.0, O.PUT), N)
+    assert q.fp64_ops == (3 * q.merge_visits + 4 * q.crossings + 2 * q.restrict_cvx
+                          + 4 * q.restrict_ncvx + 2 * q.scale_visits)
+    assert q.restrict_ncvx == 0
+    nodes = (N + 1) * (N + 2) // 2
+    # every node update restricts both parties' w/r: two scan passes over >= 1 vertex
+    assert q.restrict_cvx >= 2 * 2 * nodes and q.scale_visits >= 2 * nodes
+    qk = O.price_tc(O.Option(100.0, 100.0, 1.0, 0.2, 0.05, 0.02, O.CALL), N)
+    assert qk.restrict_ncvx > 0  # the buyer's z is non-convex (P:135-144)
+
+
+def test_kink_bins_cover_counts():
+    for c in list(range(0, 300)) + [1000, 2047, 2048, 3001, 65535, 100000]:
+        lo_bins = [b for b in range(240) if O.kink_bin_hi(b) >= c]
+        b = lo_bins[0]
+        assert O.kink_bin_hi(b) >= c and (b == 0 or O.kink_bin_hi(b - 1) < c)
