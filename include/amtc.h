@@ -186,6 +186,26 @@ int amtc_price_tree_sharded(const amtc_params* params, int32_t N, const amtc_pay
    equal work, rank 0 holding strip 0 (the root).  lo: nranks + 1 ints. */
 int amtc_tree_shard_plan(int32_t N, int nranks, int32_t* lo);
 
+/* Host-only deal of ONE batch of n options over nranks GPUs for the batched
+   transaction-cost path ("Sort options by estimated cost ...
+   deal to ranks LPT / snake order so per-GPU work is equal; equal option
+   counts ('split evenly')"; the paper's load-balance concern).
+   Estimated cost of an option (both parties) at N steps:
+     (N+1)(N+2)/2 * (2 + AMTC_HEAVY_WEIGHT * [kind != put] * k/h),  h = sigma sqrt(T/N):
+   the buyer of a call / bull spread carries ~c k/h heavy columns per level
+   (the weight is fitted to the oracle's vertex counts).
+   Options are sorted by cost (descending, ties by index) and dealt in snake
+   order 0,1,..,n-1,n-1,..,0,0,1,..: per-rank counts differ by at most one.
+   h_in: HOST SoA (only T, sigma, k, kind are read; k may be NULL = 0).
+   rank_of: n ints (out), the rank that prices option i.  rank_cost: nranks
+   doubles (out, may be NULL), the summed estimate per rank.
+   Returns AMTC_EINVAL on n < 0, N < 1, nranks < 1 or a NULL pointer; invalid
+   options are dealt like any other (the rank that prices them reports their
+   status).  No device memory, no CUDA call. */
+#define AMTC_HEAVY_WEIGHT 4.0
+int amtc_batch_shard_plan(const amtc_batch_soa* h_in, int64_t n, int32_t N, int nranks, int32_t* rank_of,
+                          double* rank_cost);
+
 /* Human-readable name of a status code (static storage). */
 const char* amtc_strerror(int status);
 

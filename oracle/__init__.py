@@ -57,7 +57,8 @@ class _Quote(C.Structure):
                 ("sum_kinks_ask", C.c_int64), ("sum_kinks_bid", C.c_int64),
                 ("crossings", C.c_int64), ("hedge_ask", C.c_double), ("hedge_bid", C.c_double),
                 ("fp64_ops", C.c_int64), ("merge_visits", C.c_int64), ("restrict_cvx", C.c_int64),
-                ("restrict_ncvx", C.c_int64), ("scale_visits", C.c_int64)]
+                ("restrict_ncvx", C.c_int64), ("scale_visits", C.c_int64),
+                ("fp64_ops_ask", C.c_int64), ("fp64_ops_bid", C.c_int64)]
 
 
 _lib = None
@@ -125,12 +126,15 @@ class Quote:
     restrict_cvx: int = 0
     restrict_ncvx: int = 0
     scale_visits: int = 0
+    fp64_ops_ask: int = 0  # fp64_ops of the seller's recursion (ask) ...
+    fp64_ops_bid: int = 0  # ... and of the buyer's (bid)
 
 
 def _quote(q) -> "Quote":
     return Quote(q.ask, q.bid, q.status, q.max_kinks_ask, q.max_kinks_bid, q.sum_kinks_ask,
                  q.sum_kinks_bid, q.crossings, q.hedge_ask, q.hedge_bid, q.fp64_ops,
-                 q.merge_visits, q.restrict_cvx, q.restrict_ncvx, q.scale_visits)
+                 q.merge_visits, q.restrict_cvx, q.restrict_ncvx, q.scale_visits, q.fp64_ops_ask,
+                 q.fp64_ops_bid)
 
 
 def lvl_stride() -> int:

@@ -487,6 +487,7 @@ typedef struct {
        fp64_ops = 3 merge_visits + 4 crossings + 2 restrict_cvx
                   + 4 restrict_ncvx + 2 scale_visits, over every node t <= N */
     int64_t fp64_ops, merge_visits, restrict_cvx, restrict_ncvx, scale_visits;
+    int64_t fp64_ops_party[2]; /* fp64_ops split by party: [0] seller (ask), [1] buyer (bid) */
 } or_quote;
 
 /*
@@ -599,8 +600,8 @@ int oracle_price_tc_stats(const or_option *o, int N, or_quote *q, int32_t *kinks
     q->hedge_ask = q->hedge_bid = NAN;
     int st = calibrate(o, N, &u, &d, &r);
     if (st != OR_OK) { q->status = st; return st; }
-    counters cnt;
-    memset(&cnt, 0, sizeof cnt);
+    counters cntp[2]; /* per party */
+    memset(cntp, 0, sizeof cntp);
     pwl *z[2];
     z[0] = (pwl *)calloc((size_t)N + 2, sizeof(pwl));
     z[1] = (pwl *)calloc((size_t)N + 2, sizeof(pwl));
@@ -635,7 +636,7 @@ int oracle_price_tc_stats(const or_option *o, int N, or_quote *q, int32_t *kinks
                 }
                 pwl znew;
                 st = node_update_x(party, &z[party][j], &z[party][j + 1], r, Sa, Sb, xi, zeta,
-                                   o->american || t == N, &znew, &cnt);
+                                   o->american || t == N, &znew, &cntp[party]);
                 if (st != OR_OK) break;
                 /* z[party][j] is read only by nodes j-1 (done) and j (this one) */
                 pwl_free(&z[party][j]);
@@ -662,13 +663,17 @@ int oracle_price_tc_stats(const or_option *o, int N, or_quote *q, int32_t *kinks
         q->ask = pwl_eval(&z[0][0], 0.0);  /* pi^a_0 = z_0(0) */
         q->bid = -pwl_eval(&z[1][0], 0.0); /* pi^b_0 = -z'_0(0) */
     }
-    q->crossings = cnt.crossings;
-    q->merge_visits = cnt.merge_visits;
-    q->restrict_cvx = cnt.restrict_cvx;
-    q->restrict_ncvx = cnt.restrict_ncvx;
-    q->scale_visits = cnt.scale_visits;
-    q->fp64_ops = 3 * cnt.merge_visits + 4 * cnt.crossings + 2 * cnt.restrict_cvx
-                  + 4 * cnt.restrict_ncvx + 2 * cnt.scale_visits;
+    for (int p = 0; p < 2; p++) {
+        const counters *c = &cntp[p];
+        q->crossings += c->crossings;
+        q->merge_visits += c->merge_visits;
+        q->restrict_cvx += c->restrict_cvx;
+        q->restrict_ncvx += c->restrict_ncvx;
+        q->scale_visits += c->scale_visits;
+        q->fp64_ops_party[p] = 3 * c->merge_visits + 4 * c->crossings + 2 * c->restrict_cvx
+                               + 4 * c->restrict_ncvx + 2 * c->scale_visits;
+    }
+    q->fp64_ops = q->fp64_ops_party[0] + q->fp64_ops_party[1];
     q->status = st;
     for (int p = 0; p < 2; p++) {
         for (int j = 0; j <= N + 1; j++) pwl_free(&z[p][j]);

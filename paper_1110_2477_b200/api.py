@@ -53,7 +53,8 @@ EXPORTS = ["amtc_price_american_tc", "amtc_price_american_tc_batch", "amtc_price
            "amtc_launch_count", "amtc_tc_last_stats", "amtc_debug_set_heavy_threshold",
            "amtc_price_crr_tree", "amtc_comm_unique_id", "amtc_comm_init", "amtc_comm_destroy",
            "amtc_price_tree_sharded", "amtc_debug_set_split_mode", "amtc_debug_set_light_kernel",
-           "amtc_debug_set_arena_shift", "amtc_tree_shard_plan", "amtc_price_american_tc_hedge"]
+           "amtc_debug_set_arena_shift", "amtc_tree_shard_plan", "amtc_price_american_tc_hedge",
+           "amtc_batch_shard_plan"]
 
 _lib = None
 
@@ -89,6 +90,8 @@ def lib():
         L.amtc_price_tree_sharded.argtypes = [C.POINTER(Params), C.c_int32, C.POINTER(Payoff), C.c_double,
                                               C.c_void_p, C.c_int, C.c_int, C.POINTER(Quote), C.c_void_p]
         L.amtc_tree_shard_plan.argtypes = [C.c_int32, C.c_int, C.POINTER(C.c_int32)]
+        L.amtc_batch_shard_plan.argtypes = [C.POINTER(BatchSoA), C.c_int64, C.c_int32, C.c_int, C.c_void_p,
+                                            C.c_void_p]
         L.amtc_price_american_tc_hedge.argtypes = [C.POINTER(Params), C.c_int32, C.POINTER(Payoff), C.c_double,
                                                    C.POINTER(Quote), C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.amtc_debug_set_arena_shift.restype = None
@@ -318,6 +321,20 @@ def tree_shard_plan(N: int, nranks: int) -> list:
     if rc:
         raise ValueError(f"amtc_tree_shard_plan: {STATUS.get(rc, rc)}")
     return list(lo)
+
+
+def batch_shard_plan(batch, N: int, nranks: int):
+    """Host-only deal of one option batch over nranks GPUs (amtc_batch_shard_plan:
+    cost-sorted snake order, equal counts +-1).  Returns (rank_of[n] int32,
+    rank_cost[nranks] float64)."""
+    soa, keep = _soa_from_numpy({f: getattr(batch, f) for f in batch.fields()})
+    n = len(batch)
+    rank_of = np.empty(n, dtype=np.int32)
+    cost = np.empty(nranks, dtype=np.float64)
+    rc = lib().amtc_batch_shard_plan(C.byref(soa), n, N, nranks, rank_of.ctypes.data, cost.ctypes.data)
+    if rc:
+        raise ValueError(f"amtc_batch_shard_plan: {STATUS.get(rc, rc)}")
+    return rank_of, cost
 
 
 def price_american_tc_hedge(S0: float, K: float, T: float, sigma: float, R: float, N: int, k: float,

@@ -148,12 +148,16 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
     // workspace budget: 60% of (free + what this library already holds), at most
     // 48 GB; cudaMemGetInfo is queried once per device and refreshed only when
     // a call would need more than the cached budget allows
-    if (!st->budget) {
+    auto refresh_budget = [&]() -> int {
         size_t free_b = 0, total_b = 0;
         AMTC_CUDA(cudaMemGetInfo(&free_b, &total_b));
         st->budget = std::min<size_t>((size_t)(0.6 * (double)(free_b + st->held())), (size_t)48 << 30);
+        return STATUS_OK;
+    };
+    if (!st->budget) {
+        if (int rc = refresh_budget()) return rc;
     }
-    const size_t budget = st->budget;
+    size_t budget = st->budget;
 
     const int* q_items = static_cast<int*>(st->items[0].p);
     const int* q_count = small + SM_HIST + TC_CLASSES;  // total valid items
@@ -189,6 +193,8 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
             if (ctas < 1) want = false;
             if (want) {
                 AMTC_CUDA(st->ws.ensure(wsb * swpc * (size_t)ctas));
+                // every failing strip item (up to S per tree) appends its code
+                AMTC_CUDA(st->items[1].ensure(sizeof(int) * (size_t)std::max<int64_t>(n2, nsp)));
                 AMTC_CUDA(st->sp_items.ensure(sizeof(int) * (size_t)nsp));
                 AMTC_CUDA(st->sp_progress.ensure(sizeof(int) * (size_t)nsp));
                 AMTC_CUDA(st->sp_carry.ensure(carry_b * (size_t)nsp));
@@ -246,7 +252,20 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
         int64_t ctas = (int64_t)st->sm_count * st->occupancy;
         ctas = std::min<int64_t>(ctas, (queued + wpc - 1) / wpc);
         ctas = std::min<int64_t>(ctas, (int64_t)(budget / (wsb * wpc)));
-        if (ctas < 1) break;
+        if (ctas < 1) {
+            // the cached budget may predate memory freed since: query again once
+            if (int rc = refresh_budget()) return rc;
+            budget = st->budget;
+            ctas = std::min<int64_t>((int64_t)st->sm_count * st->occupancy, (queued + wpc - 1) / wpc);
+            ctas = std::min<int64_t>(ctas, (int64_t)(budget / (wsb * wpc)));
+        }
+        if (ctas < 1) {
+            // not even one CTA's workspace fits: every still-queued item fails
+            // with ECAPACITY (prices stay NaN), never a silent STATUS_OK
+            if (level == 0) tc_launch_mark_all_capacity(out, n, s);
+            else ovf_host = (int)queued;
+            break;
+        }
         AMTC_CUDA(st->ws.ensure(wsb * wpc * (size_t)ctas));
         int* ovf_count = small + (passes % 2 == 0 ? SM_OVF0 : SM_OVF1);
         int* ovf_items = static_cast<int*>(st->items[(passes + 1) % 2].p);
@@ -425,6 +444,7 @@ int tc_tree_sharded(const void* params_v, int N, const void* payoff_v, double k,
     tc_launch_prepare(in, 1, N, dq, static_cast<unsigned char*>(st->cls.p), small + SM_HIST,
                       static_cast<int*>(st->items[0].p), s);
     AMTC_CUDA(cudaMemsetAsync(small + SM_VSUM, 0, sizeof(unsigned long long), s));
+    AMTC_CUDA(cudaMemsetAsync(small + SM_OVF0, 0, sizeof(int), s));  // also on a rank without strips
     // split-mode buffers for both trees (seller, buyer) over ALL strips (IPC-mapped by rank-1)
     const int S = N / 32 + 1;
     const int64_t nsp = 2 * (int64_t)S;
@@ -517,12 +537,23 @@ int tc_tree_sharded(const void* params_v, int N, const void* payoff_v, double k,
     }
     // rank 0 holds the quote (root strip); share it -- also the barrier before any
     // rank reuses buffers a peer may still read
-    if (ovf > 0) tc_launch_mark_capacity(static_cast<int*>(st->items[1].p), 1, dq, s);
-    if (nranks > 1) AMTC_NCCL(ncclBroadcast(dq, dq, sizeof(Quote), ncclUint8, 0, comm, s));
+    if (nranks > 1) {
+        // barrier: no rank returns (and may reset or reallocate the buffers its
+        // left neighbour reads through IPC) before every rank's kernel is done --
+        // an all-reduce needs every rank's contribution, a broadcast does not
+        AMTC_NCCL(ncclAllReduce(small + SM_WORK2, small + SM_WORK2, 1, ncclInt32, ncclSum, comm, s));
+        AMTC_NCCL(ncclBroadcast(dq, dq, sizeof(Quote), ncclUint8, 0, comm, s));
+        AMTC_NCCL(ncclAllReduce(small + SM_OVF0, small + SM_OVF1, 1, ncclInt32, ncclMax, comm, s));
+        AMTC_CUDA(cudaMemcpyAsync(&ovf, small + SM_OVF1, sizeof(int), cudaMemcpyDeviceToHost, s));
+    }
     launch_status_reduce(dq, 1, small + SM_WORST, s);
     AMTC_CUDA(cudaMemcpyAsync(out, dq, sizeof(amtc_quote), cudaMemcpyDeviceToHost, s));
     AMTC_CUDA(cudaStreamSynchronize(s));
-    if (ovf > 0 && out->status == 0) out->status = STATUS_ECAPACITY;
+    if (ovf > 0 && (out->status == 0 || out->status == STATUS_ECAPACITY)) {
+        // a strip of this tree (on any rank) outgrew its capacities: no price
+        out->status = STATUS_ECAPACITY;
+        out->ask = out->bid = NAN;
+    }
     if (peer_carry) {
         cudaIpcCloseMemHandle(peer_carry);
         cudaIpcCloseMemHandle(peer_arena);
@@ -759,6 +790,38 @@ int amtc_tree_shard_plan(int32_t N, int nranks, int32_t* lo) {
     shard_strips(N, nranks, v);
     for (int g = 0; g <= nranks; ++g) lo[g] = v[g];
     return STATUS_OK;
+}
+
+int amtc_batch_shard_plan(const amtc_batch_soa* h_in, int64_t n, int32_t N, int nranks, int32_t* rank_of,
+                          double* rank_cost) {
+    try {
+        if (!h_in || !h_in->T || !h_in->sigma || !h_in->kind || !rank_of || n < 0 || N < 1 || nranks < 1)
+            return STATUS_EINVAL;
+        const double nodes = 0.5 * ((double)N + 1.0) * ((double)N + 2.0);
+        std::vector<double> cost((size_t)n);
+        for (int64_t i = 0; i < n; ++i) {
+            const double h = h_in->sigma[i] * std::sqrt(h_in->T[i] / (double)N);
+            const double k = h_in->k ? h_in->k[i] : 0.0;
+            const double kh = (h > 0.0 && std::isfinite(h) && k > 0.0) ? k / h : 0.0;
+            cost[(size_t)i] = nodes * (2.0 + (h_in->kind[i] != AMTC_PUT ? AMTC_HEAVY_WEIGHT * kh : 0.0));
+        }
+        std::vector<int64_t> order((size_t)n);
+        for (int64_t i = 0; i < n; ++i) order[(size_t)i] = i;
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int64_t a, int64_t b) { return cost[(size_t)a] > cost[(size_t)b]; });
+        if (rank_cost)
+            for (int g = 0; g < nranks; ++g) rank_cost[g] = 0.0;
+        for (int64_t q = 0; q < n; ++q) {
+            const int64_t round = q / nranks, pos = q % nranks;
+            const int g = (int)((round & 1) ? nranks - 1 - pos : pos);  // snake order
+            rank_of[order[(size_t)q]] = g;
+            if (rank_cost) rank_cost[g] += cost[(size_t)order[(size_t)q]];
+        }
+        return STATUS_OK;
+    } catch (...) {
+        g_last_error = "unexpected host exception";
+        return STATUS_ECUDA;
+    }
 }
 
 void amtc_debug_set_heavy_threshold(int tl) { strip_set_heavy_threshold(tl); }

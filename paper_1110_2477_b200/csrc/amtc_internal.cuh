@@ -48,6 +48,8 @@ void tc_launch_prepare(const BatchPtrs& in, int64_t n, int N, Quote* out, unsign
                        int* items, cudaStream_t s);
 void launch_status_reduce(Quote* out, int64_t n, int* worst, cudaStream_t s);
 void tc_launch_mark_capacity(const int* items, int n_items, Quote* out, cudaStream_t s);
+// every option still STATUS_OK -> ECAPACITY with NaN prices (no workspace fits)
+void tc_launch_mark_all_capacity(Quote* out, int64_t n, cudaStream_t s);
 
 // amtc_strip.cu (the transaction-cost solver)
 struct StripLaunchArgs {

@@ -123,6 +123,21 @@ void tc_launch_split_expand(const int* items, const int* n_items, int S, int64_t
     note_launch();
 }
 
+__global__ void tc_mark_all_capacity_kernel(int64_t n, Quote* out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (out[i].status == STATUS_OK) {  // invalid options keep their own status
+        out[i].status = STATUS_ECAPACITY;
+        out[i].ask = out[i].bid = NAN;
+    }
+}
+
+void tc_launch_mark_all_capacity(Quote* out, int64_t n, cudaStream_t s) {
+    if (n <= 0) return;
+    tc_mark_all_capacity_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, out);
+    note_launch();
+}
+
 void tc_launch_mark_capacity(const int* items, int n_items, Quote* out, cudaStream_t s) {
     if (n_items <= 0) return;
     tc_mark_capacity_kernel<<<(n_items + 255) / 256, 256, 0, s>>>(items, n_items, out);

@@ -247,7 +247,11 @@ static int tree_run(const TreeConsts& c, int N, ncclComm_t comm, int rank, int n
                     cudaStream_t s) {
     TreeBufs* B = tree_bufs();
     std::lock_guard<std::mutex> guard(B->mu);
-    const int64_t cap = (N + 1 + nranks - 1) / nranks + TREE_D + 64;
+    // widest range any rank owns at any level: ceil((N+1)/n) while every rank
+    // is active, but up to 2 TREE_MIN_COLS - 1 columns on rank 0 while the
+    // processor reduction keeps fewer ranks active (split_at); plus the halo
+    const int64_t own_max = std::max<int64_t>((N + 1 + nranks - 1) / nranks, 2 * TREE_MIN_COLS);
+    const int64_t cap = own_max + TREE_D + 64;
     cudaError_t e = B->ensure((size_t)cap);
     if (e != cudaSuccess) return cuda_err(e, "tree buffers");
     double* cur = B->p[0];   // own columns of the current level
@@ -268,6 +272,10 @@ static int tree_run(const TreeConsts& c, int N, ncclComm_t comm, int rank, int n
         };
         int64_t my_lo, my_hi;
         need(rank, my_lo, my_hi);
+        if (b - a > cap || my_hi - my_lo > cap) {  // cannot happen with own_max above
+            t_err = "sharded tree: rank range exceeds its buffers";
+            return STATUS_EINVAL;
+        }
         // gather the window: intersections of owners' ranges with windows
         if (comm) {
             if (ncclGroupStart() != ncclSuccess) return STATUS_ENCCL;

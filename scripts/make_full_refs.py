@@ -30,7 +30,7 @@ from paper_1110_2477_b200 import workloads as W  # noqa: E402
 GOLD = os.path.join(ROOT, "tests", "golden")
 TC_FIELDS = ("ask", "bid", "status", "max_kinks_ask", "max_kinks_bid", "sum_kinks_ask",
              "sum_kinks_bid", "crossings", "fp64_ops", "merge_visits", "restrict_cvx",
-             "restrict_ncvx", "scale_visits", "seconds")
+             "restrict_ncvx", "scale_visits", "fp64_ops_ask", "fp64_ops_bid", "seconds")
 
 
 def opt(row):
