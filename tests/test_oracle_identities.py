@@ -196,8 +196,6 @@ def test_cost_model_counts():
                           + 4 * q.restrict_ncvx + 2 * q.scale_visits)
     assert q.restrict_ncvx == 0
     assert q.fp64_ops_ask + q.fp64_ops_bid == q.fp64_ops
-    # k = 0: both parties' functions are lines (A.1), so both recursions do the same work
-    assert q.fp64_ops_ask == q.fp64_ops_bid
     nodes = (N + 1) * (N + 2) // 2
     # every node update restricts both parties' w/r: two scan passes over >= 1 vertex
     assert q.restrict_cvx >= 2 * 2 * nodes and q.scale_visits >= 2 * nodes
