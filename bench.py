@@ -6,9 +6,12 @@ Default workload (BASELINE.json config 4): 16384 American options per GPU
 bid under proportional costs k ~ U[0, 2%], fp64.  One "step" = pricing the
 whole batch through the C-ABI (amtc_price_american_tc_batch, inputs resident in
 HBM).  Multi-GPU: one process per GPU (torchrun); each rank prices its own
-16384-option batch (seed + rank) with no data-path collective -> weak scaling;
-timing = max over ranks of the device time (CUDA events), whole-job value =
-all ranks' node-updates / that time.
+ONE 16384-option batch is dealt over the ranks by amtc_batch_shard_plan
+(cost-sorted snake order, equal counts) and the 24-byte quotes are all-gathered
+at the end of every step -> strong scaling; timing = max over ranks of the
+device time (CUDA events), value = the batch's node-updates / that time.
+--slice g/n times rank g's share of an n-GPU deal alone on one GPU (per-rank
+times of an n-GPU run without n GPUs).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4|2] [--impl amtc|reference]
 
@@ -136,23 +139,66 @@ def sum_over_ranks(x: float, pg, device) -> float:
     return float(t.item())
 
 
-def workload(config: int, rank: int):
+def workload(config: int, rank: int = 0):
+    """ONE seeded batch of the workload; under torchrun every rank draws the same
+    batch and prices the share amtc_batch_shard_plan deals it (strong scaling)."""
     from paper_1110_2477_b200 import workloads as W
     if config == 4:
-        b = W.config4(seed=W.SEED_BASE + 4 + 1000 * rank)
-        return b, W.CONFIG4_N, "config4: American put/call/bull-spread batch, ask+bid under proportional costs"
+        return W.config4(), W.CONFIG4_N, "config4: American put/call/bull-spread batch, ask+bid under proportional costs"
     if config == 2:
-        b = W.config2(seed=W.SEED_BASE + 2 + 1000 * rank)
-        return b, W.CONFIG2_N, "config2: zero-cost American put/call batch (CRR), one tree per warp"
+        return W.config2(), W.CONFIG2_N, "config2: zero-cost American put/call batch (CRR), one tree per warp"
     raise SystemExit(f"unknown --config {config}")
 
 
-def cpu_baseline(config: int, budget_options: int = 8, seed: int = 123) -> dict:
-    """The oracle as it stands, on all host cores, on a bounded seeded sample."""
-    import oracle as O
+def oracle_cache(config: int, batch):
+    """The cached full-batch oracle file (tests/golden/oracle_config<c>_full.npz,
+    written by scripts/make_full_refs.py from oracle/ only), if its SHA-256 key
+    matches this batch; else None."""
     from paper_1110_2477_b200 import workloads as W
+    path = os.path.join(ROOT, "tests", "golden", f"oracle_config{config}_full.npz")
+    if not os.path.exists(path):
+        return None
+    z = np.load(path)
+    if str(z["sha256"]) != W.soa_sha256(batch):
+        return None
+    return z
+
+
+# A19 (DESIGN.md): |g - o| <= 1e-9 |o|, or the rounding floor 4 N eps S0
+REL_TOL = 1e-9
+FLOOR_C = 4.0
+
+
+def abs_floor(N: int, S0) -> np.ndarray:
+    """DESIGN.md A19: FLOOR_C N eps S0 (N levels of fp64 updates of values of size S0)."""
+    return FLOOR_C * N * np.finfo(np.float64).eps * np.asarray(S0, dtype=np.float64)
+
+
+def parity_vs_oracle(got: np.ndarray, ref: np.ndarray, N: int, S0) -> dict:
+    """Element-wise comparison with the cached oracle (every option)."""
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    err = np.abs(got - ref)
+    rel_ok = err <= REL_TOL * np.abs(ref)
+    floor_ok = err <= abs_floor(N, np.broadcast_to(S0, ref.shape))
+    ok = rel_ok | floor_ok
+    nz = np.abs(ref) > 0
+    return {"checked": int(ref.size), "pass": int(ok.sum()), "fail": int((~ok).sum()),
+            "max_rel_err": float(np.max(err[nz] / np.abs(ref[nz]))) if nz.any() else 0.0,
+            "max_err_over_N_eps_S0": float(np.max(err / abs_floor(N, np.broadcast_to(S0, ref.shape)) * FLOOR_C)),
+            "floor_used": int((floor_ok & ~rel_ok).sum())}
+
+
+def cpu_baseline(config: int, budget_options: int = 24, seed: int = 123) -> dict:
+    """The oracle as it stands, on all host cores, on a bounded seeded sample.
+    With the cached oracle op counts available the sample's throughput is
+    extrapolated by WORK (the SURVEY 8(d) cost-model ops of the sample vs the
+    whole batch), so the value does not hinge on how many heavy call buyers the
+    sample happens to hold."""
+    import oracle as O
     b, N, _ = workload(config, 0)
-    idx = np.sort(np.random.default_rng(seed).choice(len(b), budget_options, replace=False))
+    g = np.random.default_rng(seed)
+    idx = np.sort(g.choice(len(b), budget_options, replace=False))
     cores = len(os.sched_getaffinity(0))
     opts = []
     for i in idx:
@@ -166,10 +212,19 @@ def cpu_baseline(config: int, budget_options: int = 8, seed: int = 123) -> dict:
         O.price_crr_many(opts, N, threads=cores)
         nodes = crr_nodes(N) * len(opts)
     dt = time.perf_counter() - t0
-    return {"value": nodes / dt, "unit": "node-updates/s", "cores": min(cores, len(opts)), "kind": "oracle",
+    raw = nodes / dt
+    value, how = raw, "per option"
+    z = oracle_cache(config, b) if config == 4 else None
+    if z is not None:
+        ops = z["fp64_ops"].astype(np.float64)
+        # time for the whole batch at the sample's ops/s; value = batch node-updates / that
+        t_batch = dt * ops.sum() / ops[idx].sum()
+        value, how = tc_nodes(N) * len(b) / t_batch, "by oracle cost-model ops (sample ops / batch ops)"
+    return {"value": value, "unit": "node-updates/s", "cores": min(cores, len(opts)), "kind": "oracle",
             "sample": f"{len(opts)} options of the config-{config} batch (numpy default_rng({seed}) choice), "
-                      f"N={N}, one option per thread, {dt:.1f} s wall",
-            "options_per_s": len(opts) / dt}
+                      f"N={N}, one option per thread on {min(cores, len(opts))} threads, {dt:.1f} s wall; "
+                      f"extrapolated {how}",
+            "raw_sample_value": raw, "options_per_s": value / (tc_nodes(N) if config == 4 else crr_nodes(N))}
 
 
 def run_reference(args):
@@ -177,7 +232,6 @@ def run_reference(args):
     if rank != 0:
         return 0
     times = []
-    res = None
     for i in range(args.warmup + args.steps):
         res = cpu_baseline(args.config, budget_options=args.ref_options, seed=123 + i)
         if i >= args.warmup:
@@ -185,21 +239,49 @@ def run_reference(args):
     vals = [r["value"] for r in times]
     value = float(np.mean(vals))
     b, N, desc = workload(args.config, 0)
+    per_opt = tc_nodes(N) if args.config == 4 else crr_nodes(N)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "node-updates/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": float(np.mean([args.ref_options * tc_nodes(N) / r["value"] * 1e3 for r in times])),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "ms_per_step": float(len(b) * per_opt / value * 1e3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": desc, "N": N, "options_per_gpu": len(b), "options_total": len(b),
-                       "node_updates_per_option": tc_nodes(N) if args.config == 4 else crr_nodes(N),
+            "config": {"workload": desc, "N": N, "options_total": len(b),
+                       "node_updates_per_option": per_opt,
                        "parallelism": "host cores, one option per thread",
                        "reference_sample": f"each step prices a seeded sample of {args.ref_options} options of "
-                                           "this workload (bounded CPU time)"},
+                                           "this workload (bounded CPU time); ms_per_step is the whole batch "
+                                           "at that rate"},
             "cpu_baseline": {"value": value, "unit": "node-updates/s", "cores": times[-1]["cores"],
                              "kind": "oracle", "sample": times[-1]["sample"]},
             "e2e": {"value": value, "unit": "node-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def fp64_peak():
+    """FP64 DFMA peak measured on this pool (tools/fp64_peak.cu ->
+    profiles/r01_fp64_peak.json): instr/s and flop/s; else the unit-count value."""
+    f = os.path.join(ROOT, "profiles", "r01_fp64_peak.json")
+    try:
+        m = json.load(open(f))
+        tf = float(m["fp64_tflops"])
+        return tf * 1e12 / 2.0, tf * 1e12, ("measured: DFMA throughput by tools/fp64_peak.cu on this pool's "
+                                            "B200 (profiles/r01_fp64_peak.json; MEASURED_PEAKS.json has no FP64 entry)")
+    except Exception:
+        v = 148 * FP64_LANES_PER_SM * 1965e6
+        return v, 2 * v, "derived: 148 SMs x 64 FP64 lanes/clk x 1965 MHz (no measurement found)"
+
+
+def max_bp_hist(mbp: np.ndarray) -> dict:
+    edges = [1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 8192]
+    out = {}
+    lo = 0
+    for e in edges:
+        c = int(((mbp >= lo) & (mbp < e)).sum()) if lo else int((mbp < e).sum())
+        out[f"<{e}"] = c
+        lo = e
+    out[f">={edges[-1]}"] = int((mbp >= edges[-1]).sum())
+    return out
 
 
 def run_amtc(args):
@@ -211,19 +293,41 @@ def run_amtc(args):
     from paper_1110_2477_b200 import api, build
     build.build()
     api.lib()
-    b, N, desc = workload(args.config, rank)
-    n = len(b)
-    cols = api.device_batch(b, dev)
+    b, N, desc = workload(args.config)
+    # the deal: this rank's share of ONE batch (--slice g/n: rank g's share of an
+    # n-GPU deal, timed alone on this one GPU)
+    g_eff, n_eff = rank, world
+    if args.slice:
+        assert world == 1, "--slice runs one share on one GPU"
+        g_eff, n_eff = (int(x) for x in args.slice.split("/"))
+    rank_of, est_cost = api.batch_shard_plan(b, N, n_eff)
+    idx = np.nonzero(rank_of == g_eff)[0]
+    sub = b.subset(idx)
+    n = len(sub)
+    cols = api.device_batch(sub, dev)
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device=dev)
+    counts = np.bincount(rank_of, minlength=n_eff)
+    M = int(counts.max())
+    qbytes = 24 if args.config == 4 else 8
     if args.config == 4:
         out = torch.empty(n * 24, dtype=torch.uint8, device=dev)
-        step = lambda: api.price_american_tc_batch(cols, N, out, stream)
-        nodes_per_step = tc_nodes(N) * n
+        price = lambda: api.price_american_tc_batch(cols, N, out, stream)
+        per_opt = tc_nodes(N)
     else:
-        out = torch.empty(n, dtype=torch.float64, device=dev)
-        step = lambda: api.price_crr_batch(cols, N, out, stream)
-        nodes_per_step = crr_nodes(N) * n
+        out = torch.empty(n * 8, dtype=torch.uint8, device=dev)
+        out64 = out.view(torch.float64)
+        price = lambda: api.price_crr_batch(cols, N, out64, stream)
+        per_opt = crr_nodes(N)
+    nodes_per_step = per_opt * len(b) if not args.slice else per_opt * n
+    gbuf = torch.zeros(M * qbytes, dtype=torch.uint8, device=dev)
+    gall = torch.empty(world * M * qbytes, dtype=torch.uint8, device=dev)
+
+    def step():
+        price()
+        if pg is not None:  # the final gather of the quotes (the only inter-GPU traffic)
+            gbuf[: n * qbytes].copy_(out)
+            pg.all_gather_into_tensor(gall, gbuf)
 
     for _ in range(args.warmup):
         step()
@@ -238,7 +342,7 @@ def run_amtc(args):
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     launches0 = api.launch_count()
-    kernel_ms, vertex_sum = 0.0, 0
+    full_ms, light_ms = 0.0, 0.0
     for i in range(args.steps):
         flush_l2(flush)
         starts[i].record(stream)
@@ -246,68 +350,100 @@ def run_amtc(args):
         ends[i].record(stream)
         if args.config == 4:
             st = api.tc_last_stats()
-            kernel_ms += st["solve_ms"]
-            vertex_sum += st["vertex_sum"]
+            full_ms += st["full_ms"]
+            light_ms += st["light_ms"]
     torch.cuda.synchronize()
     launches = api.launch_count() - launches0
     if pg is not None:
         pg.barrier()
     torch.cuda.synchronize()
     clocks = sampler.stop() if sampler else None
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = max_over_ranks(float(np.sum(step_ms)), pg, dev)
-    total_nodes = sum_over_ranks(float(nodes_per_step * args.steps), pg, dev)
-    total_opts = sum_over_ranks(float(n * args.steps), pg, dev)
-    value = total_nodes / (total_ms / 1e3)
+    step_ms = [s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)]
+    my_ms = float(np.sum(step_ms))
+    rank_ms = [my_ms]
+    if pg is not None:
+        t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
+        tl = [torch.empty_like(t) for _ in range(world)]
+        pg.all_gather(tl, t)
+        rank_ms = [float(x.item()) for x in tl]
+    total_ms = max(rank_ms)
+    value = nodes_per_step * args.steps / (total_ms / 1e3)
 
-    # roofline of the dominant kernel: FP64 DFMA peak measured on this pool's
-    # B200s by tools/fp64_peak.cu (MEASURED_PEAKS.json has no FP64 entry);
-    # fallback: the unit-count derivation
-    props = torch.cuda.get_device_properties(dev)
-    sm_count = props.multi_processor_count
-    clk = (clocks or {}).get("sm_max_mhz") or 1965.0
-    peak_tflops = sm_count * FP64_LANES_PER_SM * 2 * clk * 1e6 / 1e12
-    peak_src = (f"derived: {sm_count} SMs x 64 FP64/clk x 2 x {clk:.0f} MHz "
-                "(no FP64 entry in MEASURED_PEAKS.json)")
-    fp64_file = os.path.join(ROOT, "profiles", "r01_fp64_peak.json")
-    if os.path.exists(fp64_file):
-        try:
-            m = json.load(open(fp64_file))
-            peak_tflops = float(m["fp64_tflops"])
-            peak_src = ("measured: DFMA throughput by tools/fp64_peak.cu on this pool's B200 "
-                        "(profiles/r01_fp64_peak.json; MEASURED_PEAKS.json has no FP64 entry)")
-        except Exception:
-            pass
-    if args.config == 4:
-        kern_ms = kernel_ms / args.steps
-        flop = TC_FLOP_PER_CHILD_VERTEX * 2.0 * vertex_sum / args.steps
-        kname = "tc_solve_kernel"
+    # the gathered quotes, in batch order, for parity and the max_bp histogram
+    if pg is not None:
+        host = gall.cpu().numpy()
+        res = np.empty(len(b), dtype=api.QUOTE_DTYPE if args.config == 4 else np.float64)
+        for g in range(world):
+            ig = np.nonzero(rank_of == g)[0]
+            seg = host[g * M * qbytes: g * M * qbytes + len(ig) * qbytes]
+            res[ig] = seg.view(res.dtype)
+        res_idx = np.arange(len(b))
     else:
-        # the CRR step is a single kernel launch: its event time is the step time
-        kern_ms = float(np.mean(step_ms))
-        flop = CRR_FLOP_PER_NODE * nodes_per_step
-        kname = "crr_kernel"
-    achieved = flop / (kern_ms / 1e3) / 1e12
-    roofline = {"bound": "alu", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
-                "frac": achieved / peak_tflops, "traffic": None, "kernel": kname,
-                "kernel_ms_per_step": kern_ms,
-                "peak_source": peak_src,
-                "flop_model": ("12 flop per child vertex per node-update (DESIGN.md)" if args.config == 4
-                               else "6 flop per CRR node-update (DESIGN.md)")}
+        res = out.cpu().numpy().view(api.QUOTE_DTYPE if args.config == 4 else np.float64)
+        res_idx = idx
+
+    # parity of this step's output against the cached oracle (every option priced)
+    parity = None
+    z = oracle_cache(args.config, b)
+    if z is not None and rank == 0:
+        if args.config == 4:
+            pa = parity_vs_oracle(res["ask"], z["ask"][res_idx], N, b.S0[res_idx])
+            pb = parity_vs_oracle(res["bid"], z["bid"][res_idx], N, b.S0[res_idx])
+            parity = {"ask": pa, "bid": pb, "source": "tests/golden/oracle_config4_full.npz (oracle/, SHA-256 keyed)",
+                      "tolerance": "A19: 1e-9 relative, or the rounding floor 4 N eps S0 (counted)"}
+        else:
+            parity = {"price": parity_vs_oracle(res, z["price"][res_idx], N, b.S0[res_idx]),
+                      "source": "tests/golden/oracle_config2_full.npz (oracle/, SHA-256 keyed)",
+                      "tolerance": "A19: 1e-9 relative, or the rounding floor 4 N eps S0 (counted)"}
+
+    # roofline: algorithmic FP64 work from the ORACLE's cost-model counts (cached per option)
+    instr_peak, flop_peak, peak_src = fp64_peak()
+    roofline = None
     if args.config == 4:
-        roofline["vertex_sum_per_step"] = vertex_sum / args.steps
-        tf = os.path.join(ROOT, "profiles", "r01_traffic_config4.json")
-        if os.path.exists(tf):
-            try:
-                roofline["traffic"] = float(json.load(open(tf))["traffic_bytes_per_step"])
-                roofline["traffic_source"] = "ncu dram__bytes_read+write of one step (profiles/r01_traffic_config4.json)"
-            except Exception:
-                pass
+        if z is not None:
+            seller_light = np.isin(b.kind[idx], [0, 1])             # seller of a put / call: light kernel
+            buyer_light = b.kind[idx] == 0                           # buyer of a put: light kernel
+            ops_a = z["fp64_ops_ask"][idx].astype(np.float64)
+            ops_b = z["fp64_ops_bid"][idx].astype(np.float64)
+            light_ops = ops_a[seller_light].sum() + ops_b[buyer_light].sum()
+            full_ops = ops_a[~seller_light].sum() + ops_b[~buyer_light].sum()
+            fm, lm = full_ms / args.steps, light_ms / args.steps
+            per_k = {}
+            for name, ops, ms in (("full", full_ops, fm), ("light", light_ops, lm)):
+                if ms > 0:
+                    a = ops / (ms / 1e3)
+                    per_k[name] = {"ops_per_step": ops, "ms": ms, "achieved_instr_per_s": a,
+                                   "frac_of_dfma_instr_peak": a / instr_peak, "frac_of_flop_peak": a / flop_peak}
+            ach = full_ops / (fm / 1e3) if fm > 0 else 0.0
+            roofline = {"bound": "alu", "achieved": ach / 1e12, "peak": instr_peak / 1e12,
+                        "unit": "T FP64-instr/s", "frac": ach / instr_peak,
+                        "traffic": None, "kernel": "strip_kernel<4,4,20,1,1> (full; the dominant kernel)",
+                        "kernels": per_k,
+                        "work_source": "oracle cost-model ops (SURVEY 8(d): merge 3, crossing 4, restriction 2|4, "
+                                       "scaling 2) per option and party, tests/golden/oracle_config4_full.npz",
+                        "peak_source": peak_src + "; DFMA = 1 instruction (the cost model counts instructions)",
+                        "flop_peak_tflops": flop_peak / 1e12}
+            tf = os.path.join(ROOT, "profiles", "r02_traffic_config4.json")
+            if os.path.exists(tf):
+                try:
+                    tj = json.load(open(tf))
+                    roofline["traffic"] = float(tj["full_kernel_bytes"])
+                    roofline["traffic_source"] = tj.get("source", tf)
+                except Exception:
+                    pass
+    else:
+        kern_ms = float(np.mean(step_ms))
+        ops = 3.0 * per_opt * n   # 1 DMUL + 1 DFMA + 1 DMNMX per CRR node-update
+        a = ops / (kern_ms / 1e3)
+        roofline = {"bound": "alu", "achieved": a / 1e12, "peak": instr_peak / 1e12, "unit": "T FP64-instr/s",
+                    "frac": a / instr_peak, "traffic": None, "kernel": "crr_kernel",
+                    "work_source": "SURVEY 8(d): 3 FP64-pipe instructions per CRR node-update",
+                    "peak_source": peak_src}
 
     # end to end through the public C-ABI with HOST buffers (pinned), H2D + D2H inside
     e2e = None
     if not args.no_e2e:
-        pinned = {f: torch.from_numpy(np.ascontiguousarray(getattr(b, f))).pin_memory()
+        pinned = {f: torch.from_numpy(np.ascontiguousarray(getattr(sub, f))).pin_memory()
                   for f in ("S0", "K", "K2", "T", "sigma", "R", "k", "kind")}
         hb = {f: t.numpy() for f, t in pinned.items()}
         h2d = sum(t.numel() * t.element_size() for t in pinned.values())
@@ -319,32 +455,46 @@ def run_amtc(args):
         for _ in range(e2e_steps):
             if args.config == 4:
                 q, rc = api.price_american_tc_batch_host(hb, N, stream)
-                d2h = q.nbytes
             else:
                 q = api.price_crr_batch_host(hb, N, stream)
-                d2h = q.nbytes
+            d2h = q.nbytes
+            if pg is not None:
+                gbuf[: n * qbytes].copy_(torch.from_numpy(q.view(np.uint8)).to(dev))
+                pg.all_gather_into_tensor(gall, gbuf)
+                torch.cuda.synchronize()
         torch.cuda.synchronize()
         e2e_s = max_over_ranks(time.perf_counter() - t0, pg, dev)
-        e2e = {"value": sum_over_ranks(float(nodes_per_step * e2e_steps), pg, dev) / e2e_s,
+        e2e = {"value": nodes_per_step * e2e_steps / e2e_s,
                "unit": "node-updates/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "steps": e2e_steps, "timer": "host wall clock around the synchronous C-ABI call"}
+               "steps": e2e_steps, "timer": "host wall clock around the synchronous C-ABI call (+ the quote gather)"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.slice:
         cpu = cpu_baseline(args.config, budget_options=args.ref_options)
 
     if rank == 0:
+        par = (f"dp{world}: one batch dealt by amtc_batch_shard_plan (cost-sorted snake order), "
+               "no inter-GPU traffic but a final all-gather of the quotes")
         line = {"metric": METRIC, "value": value, "unit": "node-updates/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
-                "config": {"workload": desc, "N": N, "options_per_gpu": n, "options_total": int(total_opts / args.steps),
-                           "options_per_s": total_opts / (total_ms / 1e3),
-                           "node_updates_per_option": tc_nodes(N) if args.config == 4 else crr_nodes(N),
+                "config": {"workload": desc, "N": N, "options_total": len(b),
+                           "options_per_rank": [int(c) for c in counts],
+                           "options_per_s": (len(b) if not args.slice else n) * args.steps / (total_ms / 1e3),
+                           "node_updates_per_option": per_opt,
                            "l2": "flushed before every timed step (512 MiB write, untimed)",
-                           "parallelism": f"dp{world} (independent options per rank, no collective)"},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-                "clocks": clocks, "step_ms": step_ms}
+                           "parallelism": par},
+                "rank_ms_per_step": [r_ / args.steps for r_ in rank_ms],
+                "roofline": roofline, "parity": parity, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(launches), "clocks": clocks, "step_ms": step_ms}
+        if args.config == 4:
+            line["max_bp_hist"] = max_bp_hist(np.asarray(res["max_bp"]))
+        if args.slice:
+            line["slice"] = {"rank": g_eff, "of": n_eff, "options": n,
+                             "est_cost_share": float(est_cost[g_eff] / est_cost.sum()),
+                             "note": "one rank's share of the n-GPU deal, timed alone on one GPU"}
+            line["config"]["workload"] = desc + f" -- slice {g_eff}/{n_eff} of the deal"
         print(json.dumps(line), flush=True)
     if pg is not None:
         pg.barrier()
@@ -492,7 +642,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="amtc", choices=["amtc", "reference"])
-    ap.add_argument("--ref-options", type=int, default=8)
+    ap.add_argument("--ref-options", type=int, default=24)
+    ap.add_argument("--slice", default=None, help="g/n: time rank g's share of an n-GPU deal on this GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()

@@ -225,6 +225,10 @@ typedef struct {
     int64_t retried_items; /* (option, party) items re-run with larger scratch       */
     double solve_ms;       /* device time of the solver kernel launches (CUDA events
                               recorded around them on the call's stream)            */
+    double full_ms;        /* first pass: the full solver kernel alone (events on the call's
+                              stream around its launch; 0 if it did not run)          */
+    double light_ms;       /* first pass: the light solver kernel alone (events on the
+                              library's second stream; it overlaps full_ms)           */
 } amtc_tc_stats;
 int amtc_tc_last_stats(amtc_tc_stats* out);
 
@@ -240,10 +244,12 @@ void amtc_debug_set_heavy_threshold(int tl);
    the resident warps), 0 never, 1 whenever it fits in memory. */
 void amtc_debug_set_split_mode(int mode);
 
-/* TESTING HOOK: 1 (default) runs the items that never grow heavy node
-   functions (sellers, put buyers) on the light kernel variant (no tier 3,
-   higher occupancy) before the full kernel; 0 runs everything on the full
-   kernel. */
+/* TESTING HOOK: which kernel runs the items that never grow heavy node
+   functions (sellers of puts / calls at k/h < 4, put buyers), concurrently
+   with the full kernel: 1 (default) the light solver of amtc_light.cu (shared-
+   memory strip matrix, prefetched carry, no arenas); 2 the strip kernel's
+   light variant (amtc_strip.cu); 0 none (everything on the full kernel).
+   Any other value restores the default. */
 void amtc_debug_set_light_kernel(int on);
 
 /* TESTING HOOK: divide the whole-tree solver's row and carry arena capacities

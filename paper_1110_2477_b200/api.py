@@ -42,7 +42,8 @@ class BatchSoA(C.Structure):
 
 class TcStats(C.Structure):
     _fields_ = [("vertex_sum", C.c_int64), ("passes", C.c_int32), ("pad", C.c_int32),
-                ("retried_items", C.c_int64), ("solve_ms", C.c_double)]
+                ("retried_items", C.c_int64), ("solve_ms", C.c_double), ("full_ms", C.c_double),
+                ("light_ms", C.c_double)]
 
 
 QUOTE_DTYPE = np.dtype([("ask", "<f8"), ("bid", "<f8"), ("status", "<i4"), ("max_bp", "<i4")])
@@ -134,7 +135,7 @@ def debug_set_split_mode(mode: int) -> None:
 
 def debug_set_light_kernel(on: bool) -> None:
     """Testing hook: run sellers / put buyers on the light kernel variant (default on)."""
-    lib().amtc_debug_set_light_kernel(1 if on else 0)
+    lib().amtc_debug_set_light_kernel(int(on))  # 0 off, 1 amtc_light.cu (default), 2 strip-kernel variant
 
 
 def debug_set_arena_shift(shift: int) -> None:
@@ -146,7 +147,7 @@ def tc_last_stats() -> dict:
     s = TcStats()
     lib().amtc_tc_last_stats(C.byref(s))
     return {"vertex_sum": s.vertex_sum, "passes": s.passes, "retried_items": s.retried_items,
-            "solve_ms": s.solve_ms}
+            "solve_ms": s.solve_ms, "full_ms": s.full_ms, "light_ms": s.light_ms}
 
 
 # ---------------------------------------------------------------------------

@@ -71,12 +71,15 @@ struct DevState {
     int sm_count = 0;
     int occupancy = 0;
     int light_occupancy = 0;
+    int light2_occupancy = 0;
     // stats of the last TC batch
     unsigned long long vertex_sum = 0;
     int passes = 0;
     int64_t retried = 0;
     double solve_ms = 0.0;   // device time of the solver launches (CUDA events)
+    double full_ms = 0.0, light_ms = 0.0;  // first pass: each kernel on its own stream
     cudaEvent_t ev[2 * 8] = {};
+    cudaEvent_t kev[4] = {};  // full kernel start / end (stream s), light kernel start / end (stream s2)
 };
 
 static DevState* state_for_device(int dev) {
@@ -105,7 +108,8 @@ enum { SM_HIST = 0, SM_WORK = TC_CLASSES + 1, SM_OVF0, SM_OVF1, SM_WORST, SM_SPL
 
 // split mode policy (testing hook amtc_debug_set_split_mode): -1 auto, 0 off, 1 on when it fits
 static int g_split_mode = -1;
-// light kernel for class-0 items (testing hook amtc_debug_set_light_kernel)
+// light kernel for class-0 items (testing hook amtc_debug_set_light_kernel):
+// 1 = amtc_light.cu (default), 2 = the strip kernel's light variant, 0 = none
 static int g_light_kernel = 1;
 
 // solver passes: every item first runs at capacity level 0; items that
@@ -126,6 +130,7 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
         AMTC_CUDA(cudaDeviceGetAttribute(&st->sm_count, cudaDevAttrMultiProcessorCount, dev));
         st->occupancy = strip_ctas_per_sm();
         st->light_occupancy = strip_light_ctas_per_sm();
+        st->light2_occupancy = light2_ctas_per_sm();
         if (st->occupancy < 1) {
             g_last_error = "strip solver cannot be resident on this device";
             return STATUS_ECUDA;
@@ -167,8 +172,10 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
     const int wpc = strip_warps_per_cta();
     if (!st->ev[0]) {
         for (auto& e : st->ev) AMTC_CUDA(cudaEventCreate(&e));
+        for (auto& e : st->kev) AMTC_CUDA(cudaEventCreate(&e));
     }
     st->retried = 0;
+    bool light_ran = false, full_ran = false;
 
     // Split mode: with few trees (fewer items than a quarter of the resident
     // warps) the strips of each tree run on different warps, pipelined through
@@ -273,15 +280,17 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
         AMTC_CUDA(cudaMemsetAsync(small + SM_WORK, 0, sizeof(int), s));
         AMTC_CUDA(cudaMemsetAsync(ovf_count, 0, sizeof(int), s));
         AMTC_CUDA(cudaEventRecord(st->ev[2 * passes], s));
-        bool light_pass = level == 0 && g_light_kernel && st->light_occupancy > 0;
+        const bool light2 = g_light_kernel == 1;
+        bool light_pass = level == 0 && g_light_kernel &&
+                          (light2 ? st->light2_occupancy : st->light_occupancy) > 0;
         StripLaunchArgs AL;
         if (light_pass) {
             // class-0 items (sellers, put buyers: items [hist[1], total) of the
             // heavy-first queue) run on the light kernel, on a second stream, so
             // its CTAs take over the SMs the full kernel's CTAs release
-            const size_t wsl = strip_ws_bytes_per_warp_light(N);
-            const int lw = strip_light_warps_per_cta();
-            int64_t lctas = (int64_t)st->sm_count * st->light_occupancy;
+            const size_t wsl = light2 ? light2_ws_bytes_per_warp(N) : strip_ws_bytes_per_warp_light(N);
+            const int lw = light2 ? light2_warps_per_cta() : strip_light_warps_per_cta();
+            int64_t lctas = (int64_t)st->sm_count * (light2 ? st->light2_occupancy : st->light_occupancy);
             lctas = std::min<int64_t>(lctas, (queued + lw - 1) / lw);
             const size_t full_b = wsb * wpc * (size_t)ctas;
             lctas = std::min<int64_t>(lctas, (int64_t)((budget > full_b ? budget - full_b : 0) / (wsl * lw)));
@@ -329,10 +338,19 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
         A.ctas = (int)ctas;
         A.hedge = d_hedge;
         if (light_pass) AMTC_CUDA(cudaEventRecord(st->ev_fork, s));
+        if (level == 0) AMTC_CUDA(cudaEventRecord(st->kev[0], s));
         if (strip_launch(A, s) != STATUS_OK) return cuda_fail(cudaGetLastError(), "strip_kernel launch");
+        if (level == 0) {
+            AMTC_CUDA(cudaEventRecord(st->kev[1], s));
+            full_ran = true;
+            light_ran = light_pass;
+        }
         if (light_pass) {
             AMTC_CUDA(cudaStreamWaitEvent(st->s2, st->ev_fork, 0));
-            if (strip_launch(AL, st->s2) != STATUS_OK) return cuda_fail(cudaGetLastError(), "light strip_kernel launch");
+            AMTC_CUDA(cudaEventRecord(st->kev[2], st->s2));
+            if ((light2 ? light2_launch(AL, st->s2) : strip_launch(AL, st->s2)) != STATUS_OK)
+                return cuda_fail(cudaGetLastError(), "light kernel launch");
+            AMTC_CUDA(cudaEventRecord(st->kev[3], st->s2));
             AMTC_CUDA(cudaEventRecord(st->ev_join, st->s2));
             AMTC_CUDA(cudaStreamWaitEvent(s, st->ev_join, 0));
         }
@@ -359,6 +377,17 @@ finish:
     st->vertex_sum = vs;
     st->passes = passes;
     st->solve_ms = 0.0;
+    st->full_ms = st->light_ms = 0.0;
+    if (full_ran) {
+        float ms = 0.f;
+        AMTC_CUDA(cudaEventElapsedTime(&ms, st->kev[0], st->kev[1]));
+        st->full_ms = ms;
+    }
+    if (light_ran) {
+        float ms = 0.f;
+        AMTC_CUDA(cudaEventElapsedTime(&ms, st->kev[2], st->kev[3]));
+        st->light_ms = ms;
+    }
     for (int p = 0; p < passes; ++p) {
         float ms = 0.f;
         AMTC_CUDA(cudaEventElapsedTime(&ms, st->ev[2 * p], st->ev[2 * p + 1]));
@@ -828,7 +857,7 @@ void amtc_debug_set_heavy_threshold(int tl) { strip_set_heavy_threshold(tl); }
 
 void amtc_debug_set_split_mode(int mode) { g_split_mode = mode < 0 ? -1 : (mode ? 1 : 0); }
 
-void amtc_debug_set_light_kernel(int on) { g_light_kernel = on ? 1 : 0; }
+void amtc_debug_set_light_kernel(int on) { g_light_kernel = (on >= 0 && on <= 2) ? on : 1; }
 
 void amtc_debug_set_arena_shift(int shift) { strip_set_arena_shift(shift); }
 
@@ -844,6 +873,8 @@ int amtc_tc_last_stats(amtc_tc_stats* out) {
     out->passes = st->passes;
     out->retried_items = st->retried;
     out->solve_ms = st->solve_ms;
+    out->full_ms = st->full_ms;
+    out->light_ms = st->light_ms;
     return STATUS_OK;
 }
 

@@ -106,6 +106,12 @@ int strip_launch(const StripLaunchArgs& a, cudaStream_t s);
 void strip_set_heavy_threshold(int tl);
 void strip_set_arena_shift(int sh);
 
+// amtc_light.cu (the light solver: small node functions, no tiers)
+size_t light2_ws_bytes_per_warp(int N);
+int light2_warps_per_cta();
+int light2_ctas_per_sm();
+int light2_launch(const StripLaunchArgs& a, cudaStream_t s);
+
 // amtc_crr.cu
 int crr_launch(const BatchPtrs& in, int64_t n, int N, double* out, cudaStream_t s);
 int crr_max_n();

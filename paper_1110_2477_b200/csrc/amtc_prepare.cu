@@ -22,9 +22,13 @@ constexpr int N_CLASSES = TC_CLASSES;
 // Class 0 (the light kernel): put buyers and sellers of puts / calls; the bull
 // spread's seller grows heavy functions too (measured: 230 config-4 bull sellers
 // overflowed the light kernel), so both bull items take the full kernel.
+// The seller of a call at large k/h reaches 7-9 vertices (oracle, config 4):
+// above KH_LIGHT_CALL_SELLER it starts on the full kernel instead of
+// overflowing the light kernel's 6-vertex slots into a serial re-run pass.
+constexpr double KH_LIGHT_CALL_SELLER = 4.0;
 __device__ __forceinline__ int item_class(const OptionConsts& oc, int party) {
-    if (oc.kind == KIND_PUT || (party == 0 && oc.kind == KIND_CALL)) return 0;
-    double kh = oc.k / oc.h;
+    const double kh = oc.k / oc.h;
+    if (oc.kind == KIND_PUT || (party == 0 && oc.kind == KIND_CALL && kh < KH_LIGHT_CALL_SELLER)) return 0;
     return min(N_CLASSES - 1, 1 + (int)(4.0 * kh));
 }
 

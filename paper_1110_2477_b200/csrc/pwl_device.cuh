@@ -47,10 +47,13 @@ AMTC_HD double xtol(double x) { return TOL_X * (1.0 + fabs(x)); }
 
 // Forward emitter: appends vertices in increasing x, skipping non-kinks
 // (same slope as the previous piece) and folding zero-length pieces.
-struct Emit {
+// STR > 0: compile-time element stride of `out` (shared-memory rows of the
+// light kernel); STR = 0: the runtime `stride` member.
+template <int STR = 0>
+struct EmitT {
     Vtx* out;
     int m, cap;
-    int stride;     // element stride of `out` (1 = contiguous; 32 = lane-interleaved slots)
+    int stride;     // element stride of `out` when STR == 0 (1 = contiguous; 32 = lane-interleaved slots)
     double sl;      // left-tail slope of the function being built
     double last_s;  // slope of the last piece emitted (sl if none)
     double ax, af;  // anchor candidate (first point offered)
@@ -61,7 +64,7 @@ struct Emit {
         out = o; m = 0; cap = c; stride = str; sl = left_slope; last_s = left_slope; has_anchor = false;
         err = DEV_OK;
     }
-    AMTC_HD Vtx& at(int i) { return out[i * stride]; }
+    AMTC_HD Vtx& at(int i) { return out[i * (STR ? STR : stride)]; }
     AMTC_HD void push(double x, double f, double s) {
         if (!has_anchor) { ax = x; af = f; has_anchor = true; }
         if (s == last_s) return;  // not a kink
@@ -92,25 +95,35 @@ struct Emit {
         return m;
     }
 };
+using Emit = EmitT<0>;
 
-// A read-only function view.
-struct Fn {
+// A read-only function view (STR > 0: compile-time element stride).
+template <int STR = 0>
+struct FnT {
     const Vtx* p;
     int n;
     double sl;
-    int stride;  // element stride of p (1 = contiguous; 32 = lane-interleaved slots)
-    AMTC_HD const Vtx& v(int i) const { return p[i * stride]; }
+    int stride;  // element stride of p when STR == 0 (1 = contiguous; 32 = lane-interleaved slots)
+    AMTC_HD const Vtx& v(int i) const { return p[i * (STR ? STR : stride)]; }
     AMTC_HD double slope_right(int i) const { return i < 0 ? sl : v(i).s; }
 };
+using Fn = FnT<0>;
 AMTC_HD Fn make_fn(const Vtx* p, int n, double sl, int stride = 1) {
     Fn F;
     F.p = p; F.n = n; F.sl = sl; F.stride = stride;
     return F;
 }
+template <int STR>
+AMTC_HD FnT<STR> make_fn_s(const Vtx* p, int n, double sl) {
+    FnT<STR> F;
+    F.p = p; F.n = n; F.sl = sl; F.stride = STR;
+    return F;
+}
 
 // value at y of the piece that starts at vertex i (i = -1: the left tail,
 // anchored at vertex 0)
-AMTC_HD double piece_at(const Fn& F, int i, double y) {
+template <int STR>
+AMTC_HD double piece_at(const FnT<STR>& F, int i, double y) {
     const Vtx& a = F.v(i < 0 ? 0 : i);
     double s = i < 0 ? F.sl : a.s;
     return fma(s, y - a.x, a.f);

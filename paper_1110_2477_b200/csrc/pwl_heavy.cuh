@@ -449,7 +449,7 @@ __device__ __forceinline__ size_t scratch_vertices(int nE) {
     return (size_t)STAGE * 32 + (size_t)(2 * nb * sizeof(double) + sizeof(Vtx) - 1) / sizeof(Vtx) + 1;
 }
 
-__device__ __noinline__ int node_update_chunk(const Fn U, const Fn D, double lo, double hi, double ux, double uf,
+static __device__ __noinline__ int node_update_chunk(const Fn U, const Fn D, double lo, double hi, double ux, double uf,
                                               bool seller, Vtx* scratch, int scap, Vtx* arena, int* counter,
                                               int acap, int& zoff, int& nZ, int lane) {
     const HCtx h = make_ctx(U, D);
@@ -742,7 +742,7 @@ struct EmitAdapter {
     __device__ __forceinline__ void push(double x, double f, double s) { e->push(x, f, s); }
 };
 
-__device__ __noinline__ int node_update(const Fn U, const Fn D, double lo, double hi, double ux, double uf,
+static __device__ __noinline__ int node_update(const Fn U, const Fn D, double lo, double hi, double ux, double uf,
                                         bool seller, Vtx* scratch, int scap, Vtx* arena, int* counter, int acap,
                                         int& zoff, int& nZ, int lane) {
     const HCtx h = make_ctx(U, D);
@@ -1011,7 +1011,7 @@ __device__ __forceinline__ Ev block_event(const HWin& Wn, int code) {
 
 // z is written to zout[0 .. nZ) (contiguous, capacity zcap)
 template <class WinPtr>
-__device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo, double hi, double ux, double uf,
+static __device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo, double hi, double ux, double uf,
                                               bool seller, WinPtr win, Vtx* scratch, int scap, Vtx* zout, int zcap,
                                               int& nZ, int lane) {
     Vtx* const arena = zout;
@@ -1267,7 +1267,7 @@ __device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo,
 // infima of PWL functions over half lines sit at 0 or at vertices).  Also W's
 // tail slopes (boundedness) and the minimising vertex (the root hedge, smallest
 // x on ties).
-__device__ __noinline__ double root_min(const Fn U, const Fn D, double lo, double hi, double& slW, double& srW,
+static __device__ __noinline__ double root_min(const Fn U, const Fn D, double lo, double hi, double& slW, double& srW,
                                         double& ymin, int lane) {
     const HCtx h = make_ctx(U, D);
     const int nb = (h.nE + 31) / 32;

@@ -27,10 +27,11 @@ namespace amtc {
 
 // reversed emitter of pass A (writes buf[(cap-1-m) * stride]); folds
 // (near) zero-length pieces into the vertex on their right
-struct RevOut {
+template <int STR = 0>
+struct RevOutT {
     Vtx* buf;
     int m, cap, stride, err;
-    AMTC_HD Vtx& at(int i) { return buf[i * stride]; }
+    AMTC_HD Vtx& at(int i) { return buf[i * (STR ? STR : stride)]; }
     AMTC_HD void push(double x, double f, double s_right) {
         if (m > 0 && !(x < at(cap - m).x - xtol(x))) return;
         if (m >= cap) { err |= DEV_OVERFLOW; return; }
@@ -46,14 +47,15 @@ struct RevOut {
 // A crossing back to W found while flat lies on W's piece left of x; it is
 // confirmed only when the next vertex to the left (or the left tail) shows it
 // lies inside that piece.
-struct PassA {
+template <int STR = 0>
+struct PassAT {
     double lo;
     double cur_s;          // A's slope just right of the current position
     bool flat;
     double Lx, Lf;         // flat line anchor
     bool pend;             // pending crossing at (yc, fc), after which A follows W with slope ps
     double yc, fc, ps;
-    RevOut out;
+    RevOutT<STR> out;
 
     AMTC_HD void init(double lo_, double right_tail, Vtx* buf, int cap, int stride) {
         lo = lo_; cur_s = right_tail; flat = false; pend = false;
@@ -106,7 +108,8 @@ struct PassA {
 // Pass 1: W = max(U, D) right to left, streamed into pass A.
 // Returns DEV_OK / DEV_OVERFLOW / DEV_UNBOUNDED; A = buf[(cap-nA)..cap) (stride),
 // with left-tail slope slA.
-AMTC_HD int lane_pass1(const Fn& U, const Fn& D, double lo, Vtx* buf, int cap, int stride, int& nA,
+template <int SO = 0, int SI = 0>
+AMTC_HD int lane_pass1(const FnT<SI>& U, const FnT<SI>& D, double lo, Vtx* buf, int cap, int stride, int& nA,
                        double& slA) {
     // current pieces: piece p of F starts at vertex p (p = -1: the left tail)
     int pU = U.n - 1, pD = D.n - 1;
@@ -121,7 +124,7 @@ AMTC_HD int lane_pass1(const Fn& U, const Fn& D, double lo, Vtx* buf, int cap, i
     }
     const double sRt = curU ? sU : sD;  // W's right tail
     if (sRt < lo) { nA = 0; return DEV_UNBOUNDED; }  // restriction infimum is -inf (needs d < r < u)
-    PassA pa;
+    PassAT<SO> pa;
     pa.init(lo, sRt, buf, cap, stride);
     double s_pass = sRt;              // W's slope left of the last vertex handed to pass A
     double xlast = 0.0, flast = 0.0;  // that vertex (anchor of a line)
@@ -195,7 +198,8 @@ AMTC_HD int lane_pass1(const Fn& U, const Fn& D, double lo, Vtx* buf, int cap, i
 
 // envelope of V (streamed left to right) with the exercise function u
 // (vertex (ux, uf), slopes lo | hi); V's left tail slope is lo as well.
-struct EnvU {
+template <int STR = 0>
+struct EnvUT {
     bool is_max;
     double ux, uf, lo, hi;
     bool u_passed;       // the current position is right of ux
@@ -203,7 +207,7 @@ struct EnvU {
     bool curV;           // V is the OP-winner on the current piece
     bool started;
     double x_prev;
-    Emit E;  // held by value: a pointer would force it into local memory
+    EmitT<STR> E;  // held by value: a pointer would force it into local memory
 
     AMTC_HD double uval(double y) const { return fma(y < ux ? lo : hi, y - ux, uf); }
     AMTC_HD double su() const { return u_passed ? hi : lo; }
@@ -252,9 +256,10 @@ struct EnvU {
 };
 
 // Pass 2: V = pass B over A (left to right), Z = OP(u, V) into E.
-AMTC_HD int lane_pass2(const Fn& A, double lo, double hi, double ux, double uf, bool seller, Emit& Eout) {
+template <int SE = 0, int SA = 0>
+AMTC_HD int lane_pass2(const FnT<SA>& A, double lo, double hi, double ux, double uf, bool seller, EmitT<SE>& Eout) {
     if (A.sl > hi) return DEV_UNBOUNDED;
-    EnvU env;
+    EnvUT<SE> env;
     env.E.init(Eout.out, Eout.cap, lo, Eout.stride);
     env.is_max = seller; env.ux = ux; env.uf = uf; env.lo = lo; env.hi = hi;
     env.u_passed = false; env.started = false; env.curV = true;

@@ -1,10 +1,7 @@
 """GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the
-same seeded inputs.  Tolerance (north star): 1e-9 relative in fp64, plus an
-absolute floor of 1e-12 * S0 for prices at or near zero, where a relative
-bound is undefined (reading A19 in DESIGN.md: node-function values are O(S0)
-and every one of the N levels rounds them, so prices that are exactly 0 in
-the oracle come out as +-N * O(eps * S0) on any other evaluation order).
-Every option in these tests has S0 = 100."""
+same seeded inputs.  Tolerance (north star): 1e-9 relative in fp64; only where
+the oracle's price is below 1e-6 an absolute floor of 4 N eps S0 (reading A19
+in DESIGN.md, tests/tolerance.py).  Every option in these tests has S0 = 100."""
 import json
 import math
 import os
@@ -17,12 +14,7 @@ from paper_1110_2477_b200 import workloads as W
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
-RTOL = 1e-9
-ATOL = 1e-12 * 100.0  # 1e-12 * S0 (reading A19)
-
-
-def close(g, o):
-    return abs(g - o) <= RTOL * abs(o) + ATOL
+from tolerance import check_arrays, close, floor  # noqa: E402  (1e-9 relative; A19 floor only for |o| < 1e-6)
 
 
 @pytest.fixture(scope="module")
@@ -47,7 +39,7 @@ def assert_quotes(got, batch, N, want=None):
         if q.status:
             assert math.isnan(g["ask"]) and math.isnan(g["bid"])
             continue
-        if not (close(g["ask"], q.ask) and close(g["bid"], q.bid)):
+        if not (close(g["ask"], q.ask, N) and close(g["bid"], q.bid, N)):
             bad.append((i, batch.row(i), float(g["ask"]), q.ask, float(g["bid"]), q.bid))
     assert not bad, bad[:5]
 
@@ -79,7 +71,7 @@ def test_config1_single_put(api):
         q = api.price_american_tc(100.0, 100.0, 0.25, 0.2, 0.1, W.CONFIG1_N, k, api.PUT)
         o = O.price_tc(O.Option(100.0, 100.0, 0.25, 0.2, 0.1, k, O.PUT), W.CONFIG1_N)
         assert q["status"] == 0
-        assert close(q["ask"], o.ask) and close(q["bid"], o.bid), (q, o)
+        assert close(q["ask"], o.ask, W.CONFIG1_N) and close(q["bid"], o.bid, W.CONFIG1_N), (q, o)
     crr = O.price_crr(O.Option(100.0, 100.0, 0.25, 0.2, 0.1, 0.0, O.PUT), W.CONFIG1_N)
     assert abs(q["ask"] - crr) <= 1e-9 * crr and abs(q["bid"] - crr) <= 1e-9 * crr
 
@@ -106,7 +98,7 @@ def test_edge_cases(api):
     got, rc = api.price_american_tc_batch_host(b0, 100)
     for i in range(len(b0)):
         crr = O.price_crr(_opt(b0.row(i)), 100)
-        assert close(got["ask"][i], crr) and close(got["bid"][i], crr)
+        assert close(got["ask"][i], crr, 100) and close(got["bid"][i], crr, 100)
 
 
 def test_config3_sweep(api):
@@ -117,45 +109,62 @@ def test_config3_sweep(api):
         kind = p["kind"]
         q = api.price_american_tc(100.0, 100.0, 1.0, 0.2, 0.05, p["N"], p["k"], kind)
         assert q["status"] == 0, (p, q)
-        if not (close(q["ask"], p["ask"]) and close(q["bid"], p["bid"])):
+        if not (close(q["ask"], p["ask"], p["N"]) and close(q["bid"], p["bid"], p["N"])):
             bad.append((p, q))
     assert not bad, bad[:3]
 
 
-def test_config4_full_batch_sampled(api):
+def _full_ref(name, batch):
+    """Cached full-batch oracle values (scripts/make_full_refs.py, oracle/ only),
+    keyed by the SHA-256 of the batch's SoA bytes."""
+    path = os.path.join(GOLD, f"oracle_{name}_full.npz")
+    assert os.path.exists(path), f"{path} missing: run scripts/make_full_refs.py {name}"
+    z = np.load(path)
+    assert str(z["sha256"]) == W.soa_sha256(batch), "cached oracle file does not match the workload"
+    return z
+
+
+def test_config4_every_option(api):
     """BASELINE config 4 at full size (16384 options, N=1500) in the bench's
-    launch configuration; sampled outputs against stored oracle values."""
+    launch configuration: EVERY option's ask and bid against the cached oracle
+    (the paper validates its parallel output as "exactly the same figures" as the
+    sequential one)."""
     import torch
-    ref = json.load(open(os.path.join(GOLD, "oracle_config4.json")))
     b = W.config4()
+    ref = _full_ref("config4", b)
+    assert bool(ref["done"].all())
     cols = api.device_batch(b)
-    out, rc = api.price_american_tc_batch(cols, ref["N"])
+    out, rc = api.price_american_tc_batch(cols, W.CONFIG4_N)
     torch.cuda.synchronize()
     q = api.quotes_to_numpy(out)
     assert rc == 0, api.STATUS[rc]
-    assert np.all(q["status"] == 0)
-    assert np.all(np.isfinite(q["ask"])) and np.all(np.isfinite(q["bid"]))
-    assert np.all(q["ask"] >= q["bid"] - 1e-12)
-    bad = []
-    for s in ref["samples"]:
-        g = q[s["index"]]
-        if not (close(g["ask"], s["ask"]) and close(g["bid"], s["bid"])):
-            bad.append((s, float(g["ask"]), float(g["bid"])))
-    assert not bad, bad[:3]
+    assert np.all(q["status"] == 0) and np.all(ref["status"] == 0)
+    oka, fa = check_arrays(q["ask"], ref["ask"], W.CONFIG4_N, b.S0)
+    okb, fb = check_arrays(q["bid"], ref["bid"], W.CONFIG4_N, b.S0)
+    bad = np.nonzero(~(oka & okb))[0]
+    assert bad.size == 0, [(int(i), float(q["ask"][i]), float(ref["ask"][i]), float(q["bid"][i]),
+                            float(ref["bid"][i])) for i in bad[:5]]
+    # the capacity audit agrees with the oracle's vertex counts (representations
+    # may differ by rounding-made vertices, reading A20: compare with slack)
+    mk = np.maximum(ref["max_kinks_ask"], ref["max_kinks_bid"])
+    assert np.all(np.abs(q["max_bp"] - mk) <= np.maximum(4, 0.05 * mk))
+    print(f"config4: 16384 x 2 prices, floor used {fa + fb} times")
 
 
-def test_crr_config2_full_batch_sampled(api):
-    """BASELINE config 2 (65536 options, N=1024) full batch; sampled parity."""
+def test_config2_every_option(api):
+    """BASELINE config 2 (65536 options, N=1024, k=0): EVERY CRR price against
+    the cached oracle."""
     import torch
-    ref = json.load(open(os.path.join(GOLD, "oracle_config2.json")))
     b = W.config2()
+    ref = _full_ref("config2", b)
     cols = api.device_batch(b)
-    out = api.price_crr_batch(cols, ref["N"])
+    out = api.price_crr_batch(cols, W.CONFIG2_N)
     torch.cuda.synchronize()
     v = out.cpu().numpy()
-    assert np.all(np.isfinite(v)) and np.all(v >= 0)
-    bad = [(s, v[s["index"]]) for s in ref["samples"] if not close(v[s["index"]], s["price"])]
-    assert not bad, bad[:3]
+    ok, used = check_arrays(v, ref["price"], W.CONFIG2_N, b.S0)
+    bad = np.nonzero(~ok)[0]
+    assert bad.size == 0, [(int(i), float(v[i]), float(ref["price"][i])) for i in bad[:5]]
+    print(f"config2: 65536 prices, floor used {used} times")
 
 
 @pytest.mark.parametrize("N", [1, 2, 127, 128, 129, 500, 1024, 1151])
@@ -164,7 +173,7 @@ def test_crr_small_and_ragged(api, N):
     got = api.price_crr_batch_host(b, N)
     for i in range(len(b)):
         o = O.price_crr(_opt(b.row(i)), N)
-        assert close(got[i], o), (i, N, got[i], o)
+        assert close(got[i], o, N), (i, N, got[i], o)
 
 
 def test_crr_equals_tc_at_k0(api):
@@ -173,8 +182,7 @@ def test_crr_equals_tc_at_k0(api):
     crr = api.price_crr_batch_host(b, N)
     tc, rc = api.price_american_tc_batch_host(b, N)
     assert rc == 0
-    np.testing.assert_allclose(tc["ask"], crr, rtol=RTOL, atol=ATOL)
-    np.testing.assert_allclose(tc["bid"], crr, rtol=RTOL, atol=ATOL)
+    assert check_arrays(tc["ask"], crr, N)[0].all() and check_arrays(tc["bid"], crr, N)[0].all()
 
 
 @pytest.mark.parametrize("tl", [2, 5, 12])
@@ -228,8 +236,8 @@ def test_split_mode_matches_oracle(api, N):
         api.debug_set_split_mode(-1)
     assert rc == 0 and rc0 == 0
     assert_quotes(got, b, N)
-    np.testing.assert_allclose(got["ask"], ref["ask"], rtol=1e-12, atol=1e-12)
-    np.testing.assert_allclose(got["bid"], ref["bid"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(got["ask"], ref["ask"], rtol=1e-12, atol=floor(N))
+    np.testing.assert_allclose(got["bid"], ref["bid"], rtol=1e-12, atol=floor(N))
 
 
 def test_config5b_single_tree_split(api):
@@ -239,26 +247,43 @@ def test_config5b_single_tree_split(api):
     N = 1200
     q = api.price_american_tc(r["S0"], r["K"], r["T"], r["sigma"], r["R"], N, r["k"], api.PUT)
     o = O.price_tc(_opt(r), N)
-    assert q["status"] == 0 and close(q["ask"], o.ask) and close(q["bid"], o.bid), (q, o)
+    assert q["status"] == 0 and close(q["ask"], o.ask, N) and close(q["bid"], o.bid, N), (q, o)
 
 
-def test_light_kernel_matches_full_kernel(api):
-    """Sellers and put buyers run on the light kernel variant by default; the
-    full kernel must give the same prices (and both match the oracle)."""
-    b = W.random_small(64, seed=6100, k_max=0.05)
-    N = 150
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("N", [31, 64, 150])
+def test_light_kernel_matches_full_kernel(api, mode, N):
+    """Sellers and put buyers run on a light kernel by default (mode 1:
+    amtc_light.cu; mode 2: the strip kernel's light variant); the full kernel
+    must give the same prices and both must match the oracle.  N = 31 and 64
+    leave ragged / exact last strips."""
+    b = W.random_small(96, seed=6100 + N, k_max=0.05)
     try:
         api.debug_set_split_mode(0)
-        api.debug_set_light_kernel(False)
+        api.debug_set_light_kernel(0)
         ref, rc0 = api.price_american_tc_batch_host(b, N)
-        api.debug_set_light_kernel(True)
+        api.debug_set_light_kernel(mode)
         got, rc = api.price_american_tc_batch_host(b, N)
+        st = api.tc_last_stats()
     finally:
-        api.debug_set_light_kernel(True)
+        api.debug_set_light_kernel(1)
         api.debug_set_split_mode(-1)
     assert rc == 0 and rc0 == 0
-    np.testing.assert_allclose(got["ask"], ref["ask"], rtol=1e-12, atol=1e-12)
-    np.testing.assert_allclose(got["bid"], ref["bid"], rtol=1e-12, atol=1e-12)
+    assert st["light_ms"] > 0.0  # the light kernel really ran
+    np.testing.assert_allclose(got["ask"], ref["ask"], rtol=1e-12, atol=floor(N))
+    np.testing.assert_allclose(got["bid"], ref["bid"], rtol=1e-12, atol=floor(N))
+    assert_quotes(got, b, N)
+
+
+def test_call_sellers_across_kh(api):
+    """Call sellers grow 7-9 vertices at large k/h (oracle): below
+    k/h = 4 they run on the light kernel, above on the full kernel; a light-
+    kernel overflow would re-run the item on the full kernel.  All prices match."""
+    b = W.random_small(64, seed=6200, k_max=0.05)
+    b.kind[:] = W.CALL
+    N = 400
+    got, rc = api.price_american_tc_batch_host(b, N)
+    assert rc == 0
     assert_quotes(got, b, N)
 
 
@@ -269,7 +294,7 @@ def test_config5b_full_size_golden(api):
     r = W.config5b().row(0)
     q = api.price_american_tc(r["S0"], r["K"], r["T"], r["sigma"], r["R"], ref["N"], r["k"], api.PUT)
     assert q["status"] == 0
-    assert close(q["ask"], ref["ask"]) and close(q["bid"], ref["bid"]), (q, ref)
+    assert close(q["ask"], ref["ask"], ref["N"]) and close(q["bid"], ref["bid"], ref["N"]), (q, ref)
 
 
 def test_capacity_retry_passes(api):
@@ -294,8 +319,8 @@ def test_capacity_retry_passes(api):
         api.debug_set_split_mode(-1)
     assert rc0 == 0 and rc == 0
     assert st["passes"] > 1 and st["retried_items"] > 0, st
-    np.testing.assert_allclose(got["ask"], ref["ask"], rtol=1e-12, atol=1e-12)
-    np.testing.assert_allclose(got["bid"], ref["bid"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(got["ask"], ref["ask"], rtol=1e-12, atol=floor(N))
+    np.testing.assert_allclose(got["bid"], ref["bid"], rtol=1e-12, atol=floor(N))
     assert rc2 == 3 and np.any(bad["status"] == 3)  # AMTC_ECAPACITY
     assert np.all(np.isnan(bad["ask"][bad["status"] == 3]))
 
@@ -328,7 +353,7 @@ def test_root_hedge(api, N):
         g = api.price_american_tc_hedge(r["S0"], r["K"], r["T"], r["sigma"], r["R"], N, r["k"], r["kind"], r["K2"])
         o = O.price_tc(_opt(r), N)
         assert g["status"] == o.status == 0
-        assert close(g["ask"], o.ask) and close(g["bid"], o.bid), (i, g, o)
+        assert close(g["ask"], o.ask, N) and close(g["bid"], o.bid, N), (i, g, o)
         for name, gy, oy in (("ask", g["hedge_ask"], o.hedge_ask), ("bid", g["hedge_bid"], o.hedge_bid)):
             assert abs(gy - oy) <= 1e-8 * (1.0 + abs(oy)), (i, name, gy, oy, r)
 
@@ -360,7 +385,7 @@ def test_european_and_cash_variants(api, N):
         r = b.row(i)
         o = O.price_crr(O.Option(r["S0"], r["K"], r["T"], r["sigma"], r["R"], 0.0, r["kind"], r["K2"],
                                  american=not (flags[i] & 1)), N)
-        assert close(crr[i], o), (i, crr[i], o)
+        assert close(crr[i], o, N), (i, crr[i], o)
     # invalid: cash on a bull spread, unknown bit
     bad = dict(cols)
     bad["flags"] = np.where(b.kind == 2, 2, 16).astype(np.uint32)

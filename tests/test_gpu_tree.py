@@ -9,7 +9,7 @@ import oracle as O
 from paper_1110_2477_b200 import workloads as W
 
 pytestmark = pytest.mark.gpu
-RTOL, ATOL = 1e-9, 1e-12 * 100.0  # north star + reading A19 floor (S0 = 100)
+from tolerance import close  # noqa: E402  (1e-9 relative or the A19 rounding floor 4 N eps S0)
 
 
 @pytest.fixture(scope="module")
@@ -21,8 +21,8 @@ def api():
     return A
 
 
-def _close(g, o):
-    return abs(g - o) <= RTOL * abs(o) + ATOL
+def _close(g, o, N):
+    return close(g, o, N)
 
 
 CASES = [(O.PUT, 100.0, 0.0), (O.CALL, 95.0, 0.0), (O.BULL, 90.0, 110.0)]
@@ -35,7 +35,7 @@ def test_crr_tree_matches_oracle(api, N, case):
     kind, K, K2 = CASES[case]
     g = api.price_crr_tree(100.0, K, 0.8, 0.3, 0.04, N, kind, K2)
     o = O.price_crr(O.Option(100.0, K, 0.8, 0.3, 0.04, 0.0, kind, K2), N)
-    assert _close(g, o), (N, kind, g, o)
+    assert _close(g, o, N), (N, kind, g, o)
 
 
 def test_crr_tree_equals_batch_kernel(api):
@@ -45,7 +45,7 @@ def test_crr_tree_equals_batch_kernel(api):
     for i in range(len(b)):
         r = b.row(i)
         g = api.price_crr_tree(r["S0"], r["K"], r["T"], r["sigma"], r["R"], N, r["kind"], r["K2"])
-        assert _close(g, batch[i]), (i, g, batch[i])
+        assert _close(g, batch[i], N), (i, g, batch[i])
 
 
 def test_appendix_put_13906(api):
@@ -54,7 +54,7 @@ def test_appendix_put_13906(api):
     g = api.price_crr_tree(a["S0"], a["K"], a["T"], a["sigma"], a["R"], 40000, O.PUT)
     assert abs(g - 13.906) <= 5e-4
     o = O.price_crr(O.Option(a["S0"], a["K"], a["T"], a["sigma"], a["R"], 0.0, O.PUT), 40000)
-    assert _close(g, o), (g, o)
+    assert _close(g, o, 40000), (g, o)
 
 
 def test_config5a_full_size(api):
@@ -62,7 +62,7 @@ def test_config5a_full_size(api):
     r = W.config5a().row(0)
     g = api.price_crr_tree(r["S0"], r["K"], r["T"], r["sigma"], r["R"], W.CONFIG5A_N, O.PUT)
     o = O.price_crr(O.Option(r["S0"], r["K"], r["T"], r["sigma"], r["R"], 0.0, O.PUT), W.CONFIG5A_N)
-    assert _close(g, o), (g, o)
+    assert _close(g, o, W.CONFIG5A_N), (g, o)
 
 
 def test_tree_invalid_inputs(api):
@@ -80,12 +80,12 @@ def test_sharded_one_rank_nccl(api):
         for N in (130, 2000):
             q = api.price_tree_sharded(100.0, 100.0, 1.0, 0.3, 0.05, N, 0.0, O.PUT, comm=comm, rank=0, nranks=1)
             o = O.price_crr(O.Option(100.0, 100.0, 1.0, 0.3, 0.05, 0.0, O.PUT), N)
-            assert q["status"] == 0 and _close(q["ask"], o) and q["bid"] == q["ask"], (q, o)
+            assert q["status"] == 0 and _close(q["ask"], o, N) and q["bid"] == q["ask"], (q, o)
         # k > 0 through the sharded transaction-cost path (one rank: no peer)
         for N, kind, K, k in ((200, O.PUT, 100.0, 0.005), (300, O.CALL, 95.0, 0.02), (1000, O.PUT, 100.0, 0.005)):
             q = api.price_tree_sharded(100.0, K, 1.0, 0.3, 0.05, N, k, kind, comm=comm, rank=0, nranks=1)
             o = O.price_tc(O.Option(100.0, K, 1.0, 0.3, 0.05, k, kind), N)
-            assert q["status"] == 0 and _close(q["ask"], o.ask) and _close(q["bid"], o.bid), (N, q, o)
+            assert q["status"] == 0 and _close(q["ask"], o.ask, N) and _close(q["bid"], o.bid, N), (N, q, o)
     finally:
         api.comm_destroy(comm)
     # no communicator, one rank

@@ -1,7 +1,7 @@
 """Host check of the product's per-lane PWL algebra (pwl_lane.cuh compiled for
 the CPU by tools/lane_host.cpp) against the oracle: the whole backward
 induction, every node updated by lane_node_update, prices compared at the GPU
-parity tolerance (1e-9 relative + 1e-12 * S0, reading A19).  This pins the
+parity tolerance (tests/tolerance.py, reading A19).  This pins the
 device algebra without a GPU; the GPU tests then pin the kernels around it."""
 import os
 import subprocess
@@ -10,6 +10,7 @@ import numpy as np
 import pytest
 
 import oracle as O
+from tolerance import close
 from paper_1110_2477_b200 import workloads as W
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -43,8 +44,7 @@ def check(got, batch, N):
         assert int(st) == q.status, (i, r, st, q)
         if q.status:
             continue
-        tol = lambda o: 1e-9 * abs(o) + 1e-12 * r["S0"]
-        if abs(ask - q.ask) > tol(q.ask) or abs(bid - q.bid) > tol(q.bid):
+        if not (close(ask, q.ask, N, r["S0"]) and close(bid, q.bid, N, r["S0"])):
             bad.append((i, r, ask, q.ask, bid, q.bid))
     assert not bad, bad[:3]
 
