@@ -233,3 +233,67 @@ def bid_enum(S0, K, T, sigma, R, k, N, kind=PUT, K2=0.0, cost_t0=False):
             cover[i] = (-xi, -zeta)  # buyer receives (xi, zeta): Eq. (6) is Eq. (1) with -(xi, zeta)
         best = max(best, -_solve(nodes, quotes, r, N, cover))
     return best
+
+
+def bid_milp(S0, K, T, sigma, R, k, N, kind=PUT, K2=0.0, cost_t0=False, big_m=1e5):
+    """The bid as ONE mixed-integer program: the max over stopping times
+    tau of the buyer's LP, with tau encoded by binaries instead of enumerated
+    (N = 4 has 458,330 stopping times).  Per path node nu: stop_nu in {0,1},
+    alive_nu = 1 - sum of stop over the strict ancestors (alive_root = 1),
+    stop_nu <= alive_nu, stop forced (= alive) at t = N+1.  The cover rows of a
+    stop node hold exactly when stop_nu = 1 (big-M relaxation otherwise); the
+    trading rows are kept at every node (after tau the holdings are unconstrained
+    by anything else, so they never bind).  bid = max -X_root."""
+    from scipy.optimize import LinearConstraint, milp
+    nodes, quotes, r = _tree(S0, T, sigma, R, k, N, cost_t0)
+    nn = len(nodes)
+    # variables: X, Y, P, Q per node (P, Q unused at t = N+1), then stop per node
+    X = lambda i: 4 * i
+    Y = lambda i: 4 * i + 1
+    P = lambda i: 4 * i + 2
+    Q = lambda i: 4 * i + 3
+    Z = lambda i: 4 * nn + i
+    nv = 5 * nn
+    rows, lo, hi = [], [], []
+
+    def add(coefs, l, h):
+        row = np.zeros(nv)
+        for j, c in coefs:
+            row[j] += c
+        rows.append(row)
+        lo.append(l)
+        hi.append(h)
+
+    anc = {}
+    for i, (t, m, parent, path) in enumerate(nodes):
+        anc[i] = [] if parent < 0 else anc[parent] + [parent]
+    for i, (t, m, parent, path) in enumerate(nodes):
+        S, Sa, Sb = quotes[i]
+        if t <= N:
+            for s in (Sa, Sb):  # P + s (Q - Y) <= X
+                add([(P(i), 1.0), (Q(i), s), (Y(i), -s), (X(i), -1.0)], -np.inf, 0.0)
+        xi, zeta = (0.0, 0.0) if t == N + 1 else _payoff(kind, K, K2, S)
+        for s in (Sa, Sb):  # stop_i = 1  =>  X + s (Y + zeta) >= -xi
+            add([(X(i), 1.0), (Y(i), s), (Z(i), -big_m)], -xi - s * zeta - big_m, np.inf)
+        # stop_i <= alive_i = 1 - sum_{a in anc} stop_a ; '=' at t = N+1
+        coefs = [(Z(i), 1.0)] + [(Z(a), 1.0) for a in anc[i]]
+        add(coefs, 1.0 if t == N + 1 else 0.0, 1.0)
+        if parent >= 0:
+            add([(X(i), 1.0), (P(parent), -r)], 0.0, 0.0)
+            add([(Y(i), 1.0), (Q(parent), -1.0)], 0.0, 0.0)
+    add([(Y(0), 1.0)], 0.0, 0.0)
+    c = np.zeros(nv)
+    c[X(0)] = 1.0
+    lb = np.full(nv, -big_m / 10)
+    ub = np.full(nv, big_m / 10)
+    lb[4 * nn:] = 0.0
+    ub[4 * nn:] = 1.0
+    integrality = np.zeros(nv)
+    integrality[4 * nn:] = 1
+    from scipy.optimize import Bounds
+    res = milp(c, constraints=LinearConstraint(np.array(rows), np.array(lo), np.array(hi)),
+               integrality=integrality, bounds=Bounds(lb, ub),
+               options={"mip_rel_gap": 0.0, "presolve": True})
+    if res.status != 0:
+        raise RuntimeError(res.message)
+    return -res.fun

@@ -70,3 +70,24 @@ def test_cost_at_t0_matches_lp(m, k, N):
     assert abs(q.bid - bid) <= 1e-7 * scale, (q.bid, bid)
     base = O.price_tc(O.Option(S0, K, T, sigma, R, k, kind, K2), N)
     assert q.ask >= base.ask - 1e-12 and q.bid <= base.bid + 1e-12  # costs at t=0 only widen the spread
+
+
+@pytest.mark.parametrize("m,k", [(0, 0.005), (1, 0.05), (2, 0.05), (4, 0.005)])
+def test_bid_milp_n4(m, k):
+    """the bid at N = 4 against the stopping-time MILP (one binary
+    stop decision per path node, 63 of them; 458,330 stopping times are never
+    enumerated).  P:92 defines the bid as the buyer's maximal borrowing."""
+    S0, K, K2, T, sigma, R, kind = MARKETS[m]
+    q = O.price_tc(O.Option(S0, K, T, sigma, R, k, kind, K2), 4)
+    bid = B.bid_milp(S0, K, T, sigma, R, k, 4, kind, K2)
+    assert abs(q.bid - bid) <= 1e-8 * max(1.0, abs(q.ask)), (q.bid, bid)
+
+
+@pytest.mark.parametrize("N", [1, 2])
+def test_bid_milp_equals_enumeration(N):
+    """The MILP encoding of tau agrees with the exhaustive enumeration where both run."""
+    for m in (0, 1, 2):
+        S0, K, K2, T, sigma, R, kind = MARKETS[m]
+        a = B.bid_milp(S0, K, T, sigma, R, 0.02, N, kind, K2)
+        b = B.bid_enum(S0, K, T, sigma, R, 0.02, N, kind, K2)
+        assert abs(a - b) <= 1e-8 * max(1.0, abs(b))
