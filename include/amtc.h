@@ -180,6 +180,28 @@ int amtc_comm_destroy(void* comm);
 int amtc_price_tree_sharded(const amtc_params* params, int32_t N, const amtc_payoff* payoff, double k,
                             void* nccl_comm, int rank, int nranks, amtc_quote* out, void* cuda_stream);
 
+/* Host-only helper (no GPU needed): the exchange plan of band `band` (0 = the
+   top band, levels N-1 .. N-D computed from level N) of the k = 0 sharded tree
+   as rank `rank` of nranks executes it -- the very function
+   amtc_price_tree_sharded runs before each band.  D = levels per band and
+   min_cols = the processor-reduction threshold (columns per active rank,
+   P:286-288); 0 selects the library's values (256, 4096).  Rank g owns columns
+   [ceil(g w/na), ceil((g+1) w/na)) of a level of width w on the first
+   na = clamp(w/min_cols, 1, nranks) ranks, re-split every band; its
+   window at t_top is its new range plus Dp halo columns from the right (the
+   region-B dependency cone).  out (HOST): the band's levels, the
+   own / new / window column ranges [lo, hi) and `cap`, the columns of each of
+   the library's level buffers.  send / recv (HOST, 2 nranks int64 each): the
+   columns [lo, hi) of level t_top sent to / received from each peer (lo == hi:
+   none).  *n_bands (may be NULL) receives the band count; band = -1 with
+   n_bands != NULL only queries it.  Returns AMTC_EINVAL on bad arguments. */
+typedef struct {
+    int32_t t_top, Dp;
+    int64_t own_lo, own_hi, new_lo, new_hi, win_lo, win_hi, cap;
+} amtc_band;
+int amtc_tree_band_plan(int32_t N, int nranks, int rank, int32_t band, int32_t D, int64_t min_cols,
+                        amtc_band* out, int64_t* send, int64_t* recv, int32_t* n_bands);
+
 /* Host-only helper (no GPU needed): the strip partition amtc_price_tree_sharded
    uses for k > 0 -- rank g owns the 32-column strips [lo[g], lo[g+1]) of the
    N-step tree (N/32 + 1 strips, strip s carrying N - 32 s + 1 levels), ranges of

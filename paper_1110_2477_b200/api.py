@@ -46,6 +46,12 @@ class TcStats(C.Structure):
                 ("light_ms", C.c_double)]
 
 
+class Band(C.Structure):
+    _fields_ = [("t_top", C.c_int32), ("Dp", C.c_int32), ("own_lo", C.c_int64), ("own_hi", C.c_int64),
+                ("new_lo", C.c_int64), ("new_hi", C.c_int64), ("win_lo", C.c_int64), ("win_hi", C.c_int64),
+                ("cap", C.c_int64)]
+
+
 QUOTE_DTYPE = np.dtype([("ask", "<f8"), ("bid", "<f8"), ("status", "<i4"), ("max_bp", "<i4")])
 assert QUOTE_DTYPE.itemsize == C.sizeof(Quote) == 24
 
@@ -55,7 +61,7 @@ EXPORTS = ["amtc_price_american_tc", "amtc_price_american_tc_batch", "amtc_price
            "amtc_price_crr_tree", "amtc_comm_unique_id", "amtc_comm_init", "amtc_comm_destroy",
            "amtc_price_tree_sharded", "amtc_debug_set_split_mode", "amtc_debug_set_light_kernel",
            "amtc_debug_set_arena_shift", "amtc_tree_shard_plan", "amtc_price_american_tc_hedge",
-           "amtc_batch_shard_plan"]
+           "amtc_batch_shard_plan", "amtc_tree_band_plan"]
 
 _lib = None
 
@@ -91,6 +97,8 @@ def lib():
         L.amtc_price_tree_sharded.argtypes = [C.POINTER(Params), C.c_int32, C.POINTER(Payoff), C.c_double,
                                               C.c_void_p, C.c_int, C.c_int, C.POINTER(Quote), C.c_void_p]
         L.amtc_tree_shard_plan.argtypes = [C.c_int32, C.c_int, C.POINTER(C.c_int32)]
+        L.amtc_tree_band_plan.argtypes = [C.c_int32, C.c_int, C.c_int, C.c_int32, C.c_int32, C.c_int64,
+                                          C.POINTER(Band), C.c_void_p, C.c_void_p, C.POINTER(C.c_int32)]
         L.amtc_batch_shard_plan.argtypes = [C.POINTER(BatchSoA), C.c_int64, C.c_int32, C.c_int, C.c_void_p,
                                             C.c_void_p]
         L.amtc_price_american_tc_hedge.argtypes = [C.POINTER(Params), C.c_int32, C.POINTER(Payoff), C.c_double,
@@ -322,6 +330,26 @@ def tree_shard_plan(N: int, nranks: int) -> list:
     if rc:
         raise ValueError(f"amtc_tree_shard_plan: {STATUS.get(rc, rc)}")
     return list(lo)
+
+
+def tree_band_plan(N: int, nranks: int, rank: int, band: int = -1, D: int = 0, min_cols: int = 0):
+    """Host-only exchange plan of one band of the k = 0 sharded tree, as rank
+    `rank` executes it (amtc_tree_band_plan).  band = -1: the band count only.
+    Returns (plan dict, send[nranks][2], recv[nranks][2]) or the count."""
+    nb = C.c_int32(0)
+    if band < 0:
+        rc = lib().amtc_tree_band_plan(N, nranks, rank, -1, D, min_cols, None, None, None, C.byref(nb))
+        if rc:
+            raise ValueError(f"amtc_tree_band_plan: {STATUS.get(rc, rc)}")
+        return nb.value
+    b = Band()
+    snd = np.zeros((nranks, 2), dtype=np.int64)
+    rcv = np.zeros((nranks, 2), dtype=np.int64)
+    rc = lib().amtc_tree_band_plan(N, nranks, rank, band, D, min_cols, C.byref(b), snd.ctypes.data,
+                                   rcv.ctypes.data, C.byref(nb))
+    if rc:
+        raise ValueError(f"amtc_tree_band_plan: {STATUS.get(rc, rc)}")
+    return {f: getattr(b, f) for f, _ in Band._fields_}, snd, rcv
 
 
 def batch_shard_plan(batch, N: int, nranks: int):

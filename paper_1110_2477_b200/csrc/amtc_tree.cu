@@ -230,11 +230,6 @@ static TreeBufs* tree_bufs() {
 // stay on rank 0 and the rest drop out instead of exchanging halos for a few
 // columns each.  Rank g < n_act owns [ceil(g w / n_act), ceil((g+1) w / n_act)).
 constexpr int64_t TREE_MIN_COLS = 4096;
-static inline int64_t split_at(int64_t w, int g, int n) {
-    const int64_t na = std::max<int64_t>(1, std::min<int64_t>(n, w / TREE_MIN_COLS));
-    if (g >= na) return w;
-    return (g * w + na - 1) / na;
-}
 
 static thread_local std::string t_err;
 static int cuda_err(cudaError_t e, const char* what) {
@@ -242,37 +237,78 @@ static int cuda_err(cudaError_t e, const char* what) {
     return STATUS_ECUDA;
 }
 
+// The exchange plan of one band (host only; exported as amtc_tree_band_plan so
+// the multi-rank CPU test drives the library's own plan): rank `rank`'s input
+// columns [own_lo, own_hi) at t_top, its output columns [new_lo, new_hi) at
+// t_top - Dp, its window [win_lo, win_hi) at t_top (new range + Dp halo columns
+// from the right: the dependency cone) and, per peer g, the columns
+// [send[2g], send[2g+1]) of level t_top it sends to g and [recv[2g],
+// recv[2g+1]) it receives from g (empty ranges: lo == hi).  min_cols: the
+// processor-reduction threshold (columns per active rank).
+struct BandPlan {
+    int t_top, Dp;
+    int64_t own_lo, own_hi, new_lo, new_hi, win_lo, win_hi;
+};
+static void band_plan(int t_top, int D, int rank, int nranks, int64_t mc, BandPlan& P, int64_t* send, int64_t* recv) {
+    auto split = [&](int64_t w, int g) {
+        const int64_t na = std::max<int64_t>(1, std::min<int64_t>(nranks, w / mc));
+        return g >= na ? w : (g * w + na - 1) / na;
+    };
+    P.t_top = t_top;
+    P.Dp = std::min(D, t_top);
+    const int64_t w1 = t_top + 1, w0 = t_top - P.Dp + 1;
+    auto need = [&](int g, int64_t& lo, int64_t& hi) {
+        const int64_t a0 = split(w0, g), b0 = split(w0, g + 1);
+        lo = a0;
+        hi = (b0 > a0) ? std::min(b0 + P.Dp, w1) : a0;
+    };
+    P.own_lo = split(w1, rank);
+    P.own_hi = split(w1, rank + 1);
+    P.new_lo = split(w0, rank);
+    P.new_hi = split(w0, rank + 1);
+    need(rank, P.win_lo, P.win_hi);
+    for (int g = 0; g < nranks; ++g) {
+        send[2 * g] = send[2 * g + 1] = recv[2 * g] = recv[2 * g + 1] = 0;
+        if (g == rank) continue;
+        int64_t lo, hi;
+        need(g, lo, hi);
+        const int64_t s0 = std::max(lo, P.own_lo), s1 = std::min(hi, P.own_hi);
+        if (s1 > s0) { send[2 * g] = s0; send[2 * g + 1] = s1; }
+        const int64_t ga = split(w1, g), gb = split(w1, g + 1);
+        const int64_t r0 = std::max(P.win_lo, ga), r1 = std::min(P.win_hi, gb);
+        if (r1 > r0) { recv[2 * g] = r0; recv[2 * g + 1] = r1; }
+    }
+}
+// columns of each of the three level buffers: the widest own range or window
+// of any band (checked against every band by the CPU test through
+// amtc_tree_band_plan): ceil((N+1)/n) while every rank is active, up to
+// 2 min_cols - 1 on rank 0 while fewer are (processor reduction), + the halo
+static int64_t tree_cap(int N, int nranks, int D, int64_t mc) {
+    return std::max<int64_t>((N + 1 + nranks - 1) / nranks, 2 * mc) + D + 64;
+}
+
 // the whole tree, ranks 0..n-1 of comm (comm == nullptr: one GPU, no NCCL)
 static int tree_run(const TreeConsts& c, int N, ncclComm_t comm, int rank, int nranks, double* price,
                     cudaStream_t s) {
     TreeBufs* B = tree_bufs();
     std::lock_guard<std::mutex> guard(B->mu);
-    // widest range any rank owns at any level: ceil((N+1)/n) while every rank
-    // is active, but up to 2 TREE_MIN_COLS - 1 columns on rank 0 while the
-    // processor reduction keeps fewer ranks active (split_at); plus the halo
-    const int64_t own_max = std::max<int64_t>((N + 1 + nranks - 1) / nranks, 2 * TREE_MIN_COLS);
-    const int64_t cap = own_max + TREE_D + 64;
+    const int64_t cap = tree_cap(N, nranks, TREE_D, TREE_MIN_COLS);
     cudaError_t e = B->ensure((size_t)cap);
     if (e != cudaSuccess) return cuda_err(e, "tree buffers");
     double* cur = B->p[0];   // own columns of the current level
     double* win = B->p[1];   // input window of the band
     double* nxt = B->p[2];   // own columns of the next level
+    std::vector<int64_t> snd(2 * (size_t)nranks), rcv(2 * (size_t)nranks);
     // leaves (t = N), own range
-    int64_t a = split_at(N + 1, rank, nranks), b = split_at(N + 1, rank + 1, nranks);
-    launch_leaves(c, N, a, b - a, cur, s);
+    BandPlan P;
+    band_plan(N, TREE_D, rank, nranks, TREE_MIN_COLS, P, snd.data(), rcv.data());
+    launch_leaves(c, N, P.own_lo, P.own_hi - P.own_lo, cur, s);
     for (int t_top = N; t_top > 0;) {
-        const int Dp = std::min(TREE_D, t_top);
+        band_plan(t_top, TREE_D, rank, nranks, TREE_MIN_COLS, P, snd.data(), rcv.data());
+        const int Dp = P.Dp;
         const int t_bot = t_top - Dp;
-        const int64_t w1 = t_top + 1, w0 = t_bot + 1;
-        // every rank's window [lo, hi) at t_top (empty if it owns nothing at t_bot)
-        auto need = [&](int g, int64_t& lo, int64_t& hi) {
-            const int64_t a0 = split_at(w0, g, nranks), b0 = split_at(w0, g + 1, nranks);
-            lo = a0;
-            hi = (b0 > a0) ? std::min(b0 + Dp, w1) : a0;
-        };
-        int64_t my_lo, my_hi;
-        need(rank, my_lo, my_hi);
-        if (b - a > cap || my_hi - my_lo > cap) {  // cannot happen with own_max above
+        const int64_t a = P.own_lo, b = P.own_hi, my_lo = P.win_lo, my_hi = P.win_hi;
+        if (b - a > cap || my_hi - my_lo > cap || P.new_hi - P.new_lo > cap) {  // cannot happen (tree_cap)
             t_err = "sharded tree: rank range exceeds its buffers";
             return STATUS_EINVAL;
         }
@@ -280,23 +316,13 @@ static int tree_run(const TreeConsts& c, int N, ncclComm_t comm, int rank, int n
         if (comm) {
             if (ncclGroupStart() != ncclSuccess) return STATUS_ENCCL;
         }
-        for (int h = 0; h < nranks; ++h) {
-            const int64_t ha = split_at(w1, h, nranks), hb = split_at(w1, h + 1, nranks);
-            if (h == rank) {
-                // sends of my range to the others' windows
-                for (int g = 0; g < nranks; ++g) {
-                    if (g == rank) continue;
-                    int64_t lo, hi;
-                    need(g, lo, hi);
-                    const int64_t x0 = std::max(lo, ha), x1 = std::min(hi, hb);
-                    if (x1 > x0 && ncclSend(cur + (x0 - ha), (size_t)(x1 - x0), ncclDouble, g, comm, s) != ncclSuccess)
-                        return STATUS_ENCCL;
-                }
-            } else {
-                const int64_t x0 = std::max(my_lo, ha), x1 = std::min(my_hi, hb);
-                if (x1 > x0 && ncclRecv(win + (x0 - my_lo), (size_t)(x1 - x0), ncclDouble, h, comm, s) != ncclSuccess)
-                    return STATUS_ENCCL;
-            }
+        for (int g = 0; g < nranks; ++g) {
+            if (g == rank) continue;
+            const int64_t s0 = snd[2 * g], s1 = snd[2 * g + 1], r0 = rcv[2 * g], r1 = rcv[2 * g + 1];
+            if (s1 > s0 && ncclSend(cur + (s0 - a), (size_t)(s1 - s0), ncclDouble, g, comm, s) != ncclSuccess)
+                return STATUS_ENCCL;
+            if (r1 > r0 && ncclRecv(win + (r0 - my_lo), (size_t)(r1 - r0), ncclDouble, g, comm, s) != ncclSuccess)
+                return STATUS_ENCCL;
         }
         if (comm) {
             if (ncclGroupEnd() != ncclSuccess) return STATUS_ENCCL;
@@ -309,11 +335,8 @@ static int tree_run(const TreeConsts& c, int N, ncclComm_t comm, int rank, int n
                 if (e != cudaSuccess) return cuda_err(e, "window copy");
             }
         }
-        const int64_t a0 = split_at(w0, rank, nranks), b0 = split_at(w0, rank + 1, nranks);
-        launch_band(c, N, t_top, Dp, win, my_lo, my_hi - my_lo, nxt, a0, b0 - a0, s);
+        launch_band(c, N, t_top, Dp, win, my_lo, my_hi - my_lo, nxt, P.new_lo, P.new_hi - P.new_lo, s);
         std::swap(cur, nxt);
-        a = a0;
-        b = b0;
         t_top = t_bot;
     }
     // the root column belongs to rank 0; share it
@@ -371,6 +394,28 @@ int amtc_comm_init(const unsigned char id[128], int nranks, int rank, void** com
 int amtc_comm_destroy(void* comm) {
     if (!comm) return STATUS_EINVAL;
     return ncclCommDestroy(static_cast<ncclComm_t>(comm)) == ncclSuccess ? STATUS_OK : STATUS_ENCCL;
+}
+
+int amtc_tree_band_plan(int32_t N, int nranks, int rank, int32_t band, int32_t D, int64_t min_cols,
+                        amtc_band* out, int64_t* send, int64_t* recv, int32_t* n_bands) {
+    if (N < 1 || nranks < 1 || rank < 0 || rank >= nranks || D < 0 || min_cols < 0) return STATUS_EINVAL;
+    if (D == 0) D = TREE_D;
+    if (min_cols == 0) min_cols = TREE_MIN_COLS;
+    const int32_t nb = (N + D - 1) / D;
+    if (n_bands) *n_bands = nb;
+    if (band < 0 || band >= nb || !out || !send || !recv) return (band == -1 && n_bands) ? STATUS_OK : STATUS_EINVAL;
+    BandPlan P;
+    band_plan(N - band * D, D, rank, nranks, min_cols, P, send, recv);
+    out->t_top = P.t_top;
+    out->Dp = P.Dp;
+    out->own_lo = P.own_lo;
+    out->own_hi = P.own_hi;
+    out->new_lo = P.new_lo;
+    out->new_hi = P.new_hi;
+    out->win_lo = P.win_lo;
+    out->win_hi = P.win_hi;
+    out->cap = tree_cap(N, nranks, D, min_cols);
+    return STATUS_OK;
 }
 
 int amtc_price_tree_sharded(const amtc_params* params, int32_t N, const amtc_payoff* payoff, double k,
