@@ -274,6 +274,23 @@ void amtc_debug_set_split_mode(int mode);
    Any other value restores the default. */
 void amtc_debug_set_light_kernel(int on);
 
+/* TESTING HOOK: which kernel runs the whole-tree items that may grow heavy
+   node functions (buyers of calls / bull spreads, bull-spread sellers, and
+   every item when the light kernel is off): 1 (default) the full solver of
+   amtc_full.cu (strip matrix in shared memory, row / carry arenas, tier-3
+   CTA work sharing); 0 the strip kernel of amtc_strip.cu (the round-1
+   solver, still the split-mode and sharded-tree kernel).  Any other value
+   restores the default. */
+void amtc_debug_set_full_kernel(int which);
+
+/* DEVELOPER HOOK: the full solver's clock64 phase accumulators (summed over
+   warps since the last reset; out: 8 uint64, HOST): [0] cycles inside heavy
+   node updates served, [1] cycles an owner waited for its posted heavy nodes
+   (serving excluded), [2] end-of-work idle cycles, [3] total warp cycles, [4]
+   heavy nodes served, [5] levels with posted nodes, [6] tier-2 cycles.  Only a
+   build with -DAMTC_F_PROF=1 records them (else returns AMTC_EINVAL). */
+int amtc_debug_full_profile(uint64_t out[8], int reset);
+
 /* TESTING HOOK: divide the whole-tree solver's row and carry arena capacities
    by 2^shift (0 restores them), so tests can drive items through the capacity
    retry passes (4x arenas per retry) and, past the last retry, AMTC_ECAPACITY. */

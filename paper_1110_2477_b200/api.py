@@ -59,7 +59,7 @@ EXPORTS = ["amtc_price_american_tc", "amtc_price_american_tc_batch", "amtc_price
            "amtc_price_crr_batch", "amtc_price_crr_batch_host", "amtc_strerror", "amtc_last_error",
            "amtc_launch_count", "amtc_tc_last_stats", "amtc_debug_set_heavy_threshold",
            "amtc_price_crr_tree", "amtc_comm_unique_id", "amtc_comm_init", "amtc_comm_destroy",
-           "amtc_price_tree_sharded", "amtc_debug_set_split_mode", "amtc_debug_set_light_kernel",
+           "amtc_price_tree_sharded", "amtc_debug_set_split_mode", "amtc_debug_set_light_kernel", "amtc_debug_set_full_kernel", "amtc_debug_full_profile",
            "amtc_debug_set_arena_shift", "amtc_tree_shard_plan", "amtc_price_american_tc_hedge",
            "amtc_batch_shard_plan", "amtc_tree_band_plan"]
 
@@ -105,6 +105,9 @@ def lib():
                                                    C.POINTER(Quote), C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.amtc_debug_set_arena_shift.restype = None
         L.amtc_debug_set_arena_shift.argtypes = [C.c_int]
+        L.amtc_debug_full_profile.argtypes = [C.c_void_p, C.c_int]
+        L.amtc_debug_set_full_kernel.restype = None
+        L.amtc_debug_set_full_kernel.argtypes = [C.c_int]
         L.amtc_debug_set_light_kernel.restype = None
         L.amtc_debug_set_light_kernel.argtypes = [C.c_int]
         L.amtc_debug_set_split_mode.restype = None
@@ -144,6 +147,21 @@ def debug_set_split_mode(mode: int) -> None:
 def debug_set_light_kernel(on: bool) -> None:
     """Testing hook: run sellers / put buyers on the light kernel variant (default on)."""
     lib().amtc_debug_set_light_kernel(int(on))  # 0 off, 1 amtc_light.cu (default), 2 strip-kernel variant
+
+
+def debug_set_full_kernel(which: int) -> None:
+    """Testing hook: 1 the full solver of amtc_full.cu (default), 0 the strip kernel."""
+    lib().amtc_debug_set_full_kernel(int(which))
+
+
+def debug_full_profile(reset: bool = True):
+    """Developer hook: the full solver's phase counters (None unless built with -DAMTC_F_PROF=1)."""
+    out = np.zeros(8, dtype=np.uint64)
+    rc = lib().amtc_debug_full_profile(out.ctypes.data, int(reset))
+    if rc:
+        return None
+    keys = ("heavy_cycles", "wait_cycles", "idle_cycles", "total_cycles", "served", "post_levels", "tier2_cycles", "r7")
+    return {k: int(v) for k, v in zip(keys, out)}
 
 
 def debug_set_arena_shift(shift: int) -> None:

@@ -9,8 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libamtc.so")
-SOURCES = ["amtc_capi.cu", "amtc_prepare.cu", "amtc_strip.cu", "amtc_light.cu", "amtc_crr.cu", "amtc_tree.cu"]
-HEADERS = ["amtc_internal.cuh", "amtc_option.cuh", "pwl_device.cuh", "pwl_lane.cuh", "pwl_heavy.cuh"]
+SOURCES = ["amtc_capi.cu", "amtc_prepare.cu", "amtc_strip.cu", "amtc_light.cu", "amtc_full.cu", "amtc_crr.cu", "amtc_tree.cu"]
+HEADERS = ["amtc_internal.cuh", "amtc_option.cuh", "pwl_device.cuh", "pwl_lane.cuh", "pwl_heavy.cuh", "amtc_root.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

@@ -72,6 +72,7 @@ struct DevState {
     int occupancy = 0;
     int light_occupancy = 0;
     int light2_occupancy = 0;
+    int full_occupancy = 0;
     // stats of the last TC batch
     unsigned long long vertex_sum = 0;
     int passes = 0;
@@ -111,6 +112,9 @@ static int g_split_mode = -1;
 // light kernel for class-0 items (testing hook amtc_debug_set_light_kernel):
 // 1 = amtc_light.cu (default), 2 = the strip kernel's light variant, 0 = none
 static int g_light_kernel = 1;
+// the whole-tree solver for the other items (testing hook amtc_debug_set_full_kernel):
+// 1 = amtc_full.cu (default), 0 = the strip kernel (amtc_strip.cu)
+static int g_full_kernel = 1;
 
 // solver passes: every item first runs at capacity level 0; items that
 // overflowed a capacity (arena, scratch) are re-run at the next level (4x the
@@ -131,7 +135,8 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
         st->occupancy = strip_ctas_per_sm();
         st->light_occupancy = strip_light_ctas_per_sm();
         st->light2_occupancy = light2_ctas_per_sm();
-        if (st->occupancy < 1) {
+        st->full_occupancy = full_ctas_per_sm();
+        if (st->occupancy < 1 || st->full_occupancy < 1) {
             g_last_error = "strip solver cannot be resident on this device";
             return STATUS_ECUDA;
         }
@@ -170,6 +175,9 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
     int ovf_host = 0;
     int passes = 0;
     const int wpc = strip_warps_per_cta();
+    const bool full2 = g_full_kernel == 1;
+    const int fwpc = full2 ? full_warps_per_cta() : wpc;
+    const int focc = full2 ? st->full_occupancy : st->occupancy;
     if (!st->ev[0]) {
         for (auto& e : st->ev) AMTC_CUDA(cudaEventCreate(&e));
         for (auto& e : st->kev) AMTC_CUDA(cudaEventCreate(&e));
@@ -255,15 +263,16 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
         }
     }
     for (int level = 0; level <= kMaxLevel; ++level) {
-        const size_t wsb = strip_ws_bytes_per_warp(N, level);
-        int64_t ctas = (int64_t)st->sm_count * st->occupancy;
+        const int wpc = fwpc;
+        const size_t wsb = full2 ? full_ws_bytes_per_warp(N, level) : strip_ws_bytes_per_warp(N, level);
+        int64_t ctas = (int64_t)st->sm_count * focc;
         ctas = std::min<int64_t>(ctas, (queued + wpc - 1) / wpc);
         ctas = std::min<int64_t>(ctas, (int64_t)(budget / (wsb * wpc)));
         if (ctas < 1) {
             // the cached budget may predate memory freed since: query again once
             if (int rc = refresh_budget()) return rc;
             budget = st->budget;
-            ctas = std::min<int64_t>((int64_t)st->sm_count * st->occupancy, (queued + wpc - 1) / wpc);
+            ctas = std::min<int64_t>((int64_t)st->sm_count * focc, (queued + wpc - 1) / wpc);
             ctas = std::min<int64_t>(ctas, (int64_t)(budget / (wsb * wpc)));
         }
         if (ctas < 1) {
@@ -339,7 +348,8 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
         A.hedge = d_hedge;
         if (light_pass) AMTC_CUDA(cudaEventRecord(st->ev_fork, s));
         if (level == 0) AMTC_CUDA(cudaEventRecord(st->kev[0], s));
-        if (strip_launch(A, s) != STATUS_OK) return cuda_fail(cudaGetLastError(), "strip_kernel launch");
+        if ((full2 ? full_launch(A, s) : strip_launch(A, s)) != STATUS_OK)
+            return cuda_fail(cudaGetLastError(), "full solver launch");
         if (level == 0) {
             AMTC_CUDA(cudaEventRecord(st->kev[1], s));
             full_ran = true;
@@ -857,6 +867,10 @@ void amtc_debug_set_heavy_threshold(int tl) { strip_set_heavy_threshold(tl); }
 
 void amtc_debug_set_split_mode(int mode) { g_split_mode = mode < 0 ? -1 : (mode ? 1 : 0); }
 
+int amtc_debug_full_profile(uint64_t out[8], int reset) {
+    return full_profile(reinterpret_cast<unsigned long long*>(out), reset);
+}
+void amtc_debug_set_full_kernel(int which) { g_full_kernel = (which == 0) ? 0 : 1; }
 void amtc_debug_set_light_kernel(int on) { g_light_kernel = (on >= 0 && on <= 2) ? on : 1; }
 
 void amtc_debug_set_arena_shift(int shift) { strip_set_arena_shift(shift); }

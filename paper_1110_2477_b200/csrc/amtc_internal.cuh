@@ -105,6 +105,16 @@ int strip_ctas_per_sm();
 int strip_launch(const StripLaunchArgs& a, cudaStream_t s);
 void strip_set_heavy_threshold(int tl);
 void strip_set_arena_shift(int sh);
+// the capacities (vertices) of capacity level `level` (arena shift and heavy
+// threshold testing hooks applied), shared by the full solver
+void strip_tc_caps(int N, int level, int& rarena, int& carena, int& hscr, int& zbuf, int& tl);
+
+// amtc_full.cu (the full solver of the batched path: strip matrix + arenas + tier 3)
+size_t full_ws_bytes_per_warp(int N, int level);
+int full_warps_per_cta();
+int full_ctas_per_sm();
+int full_launch(const StripLaunchArgs& a, cudaStream_t s);
+int full_profile(unsigned long long out[8], int reset);
 
 // amtc_light.cu (the light solver: small node functions, no tiers)
 size_t light2_ws_bytes_per_warp(int N);

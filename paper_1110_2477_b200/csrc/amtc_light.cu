@@ -25,6 +25,7 @@
 #include "pwl_device.cuh"
 #include "pwl_heavy.cuh"
 #include "pwl_lane.cuh"
+#include "amtc_root.cuh"
 
 namespace amtc {
 
@@ -91,8 +92,6 @@ struct LightLaunch {
     double* hedge;
 };
 
-// a6 (root, P:159 / A.4): the full kernel's formula (amtc_strip.cu root_phase)
-__device__ __noinline__ int light_root(Fn mine, OptionConsts oc, bool seller, Quote* q, double* hedge, int lane);
 
 template <int C, int B, int WARPS, int MINB>
 __global__ void __launch_bounds__(WARPS * 32, MINB) light_kernel(const __grid_constant__ LightLaunch L) {
@@ -234,7 +233,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) light_kernel(const __grid_co
             if (err) break;
             if (s == 0) {
                 const Fn mine = make_fn(&S.row[lane], my_n, my_sl, LW);
-                err |= light_root(mine, oc, seller, &L.out[opt],
+                err |= tc_root(mine, oc, seller, &L.out[opt],
                                   L.hedge ? &L.hedge[2 * opt + (seller ? 0 : 1)] : nullptr, lane);
             }
             __syncwarp();
@@ -257,39 +256,6 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) light_kernel(const __grid_co
         }
         __syncwarp();
     }
-}
-
-// ---------------------------------------------------------------------------
-// a6 root for the light kernel: the same formula as the full kernel's
-// root_phase (amtc_strip.cu): v_0 is a line (no costs at t = 0; A.4)
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ Fn lshfl_fn(const Fn& F, int src) {
-    Fn G;
-    G.p = reinterpret_cast<const Vtx*>(__shfl_sync(LFULL, reinterpret_cast<unsigned long long>(F.p), src));
-    G.n = __shfl_sync(LFULL, F.n, src);
-    G.sl = __shfl_sync(LFULL, F.sl, src);
-    G.stride = __shfl_sync(LFULL, F.stride, src);
-    return G;
-}
-
-__device__ __noinline__ int light_root(Fn mine, OptionConsts oc, bool seller, Quote* q, double* hedge, int lane) {
-    const Fn Ur = lshfl_fn(mine, 0), Dr = lshfl_fn(mine, 1);
-    const bool c0 = (oc.flags & FLAG_COST_T0) != 0;
-    const double lo = c0 ? -(1.0 + oc.k) * oc.S0 : -oc.S0, hi = c0 ? -(1.0 - oc.k) * oc.S0 : -oc.S0;
-    double slW, srW, ymin;
-    const double v0 = heavy::root_min(Ur, Dr, lo, hi, slW, srW, ymin, lane);
-    if (!(slW - hi < 0.0) || !(srW - lo > 0.0)) return DEV_UNBOUNDED;
-    if (lane == 0) {
-        double xi, zeta;
-        option_payoff(oc, oc.S0, xi, zeta);
-        const double ua = xi + (0.0 < zeta ? lo : hi) * (0.0 - zeta);
-        const double ub = -xi + (0.0 < -zeta ? lo : hi) * (0.0 + zeta);
-        const bool euro = (oc.flags & FLAG_EUROPEAN) != 0;
-        if (seller) q->ask = euro ? v0 : fmax(ua, v0);  // pi^a = z_0(0)
-        else q->bid = -(euro ? v0 : fmin(ub, v0));      // pi^b = -z'_0(0)
-        if (hedge) *hedge = c0 ? NAN : ymin;            // NEXT #2
-    }
-    return DEV_OK;
 }
 
 // ---------------------------------------------------------------------------

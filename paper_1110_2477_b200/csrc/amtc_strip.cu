@@ -43,6 +43,7 @@
 #include "pwl_device.cuh"
 #include "pwl_heavy.cuh"
 #include "pwl_lane.cuh"
+#include "amtc_root.cuh"
 
 namespace amtc {
 
@@ -203,14 +204,6 @@ __device__ __forceinline__ void copy_fn(Vtx* dst, int dstride, const Vtx* src, i
 
 constexpr unsigned FULL = 0xffffffffu;
 
-__device__ __forceinline__ Fn shfl_fn(const Fn& F, int src) {
-    Fn G;
-    G.p = reinterpret_cast<const Vtx*>(__shfl_sync(FULL, reinterpret_cast<unsigned long long>(F.p), src));
-    G.n = __shfl_sync(FULL, F.n, src);
-    G.sl = __shfl_sync(FULL, F.sl, src);
-    G.stride = __shfl_sync(FULL, F.stride, src);
-    return G;
-}
 
 // tier 3 (work sharing inside the CTA): a warp whose level has heavy nodes
 // posts them (HMail per lane, bit mask `post`) and then serves posted nodes --
@@ -302,32 +295,6 @@ __device__ __noinline__ bool serve_one(CtaHdr& H, StripSmem<C, B, true>* all, in
     }
     __syncwarp();
     return true;
-}
-
-// a6: root, t = 0, no costs (derived A.4): v_0(y) = min_b [w_0(b) + S0 b] - S0 y
-// over the vertices b of w_0 = max(z_{1,0}, z_{1,1}); returns the status bits.
-__device__ __noinline__ int root_phase(Fn mine, OptionConsts oc, bool seller, Quote* q, double* hedge, int lane) {
-    const Fn Ur = shfl_fn(mine, 0), Dr = shfl_fn(mine, 1);
-    // quotes at t = 0: S0 both ways, or (1 +- k) S0 with AMTC_COST_AT_T0 (NEXT #3)
-    const bool c0 = (oc.flags & FLAG_COST_T0) != 0;
-    const double lo = c0 ? -(1.0 + oc.k) * oc.S0 : -oc.S0, hi = c0 ? -(1.0 - oc.k) * oc.S0 : -oc.S0;
-    double slW, srW, ymin;
-    const double v0 = heavy::root_min(Ur, Dr, lo, hi, slW, srW, ymin, lane);
-    // the infimum is finite iff W - hi y decreases on the left and W - lo y increases on the right
-    if (!(slW - hi < 0.0) || !(srW - lo > 0.0)) return DEV_UNBOUNDED;
-    if (lane == 0) {
-        double xi, zeta;
-        option_payoff(oc, oc.S0, xi, zeta);
-        // u_0(0) of the seller (vertex (zeta, xi)) / buyer (vertex (-zeta, -xi)), slopes lo | hi;
-        // a European option cannot be exercised at t = 0
-        const double ua = xi + (0.0 < zeta ? lo : hi) * (0.0 - zeta);
-        const double ub = -xi + (0.0 < -zeta ? lo : hi) * (0.0 + zeta);
-        const bool euro = (oc.flags & FLAG_EUROPEAN) != 0;
-        if (seller) q->ask = euro ? v0 : fmax(ua, v0);    // pi^a = z_0(0)
-        else q->bid = -(euro ? v0 : fmin(ub, v0));        // pi^b = -z'_0(0)
-        if (hedge) *hedge = c0 ? NAN : ymin;              // the position taken at t = 0 (NEXT #2)
-    }
-    return DEV_OK;
 }
 
 template <int C, int B, int WARPS, int MINB, bool HEAVY>
@@ -608,7 +575,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
             if (s == 0 && !err) {
                 const Fn mine = (my_off < 0) ? make_fn(&S.row[lane], my_n, my_sl, SW)
                                              : make_fn(WS(Vtx, rarena, cur) + my_off, my_n, my_sl, 1);
-                err |= root_phase(mine, oc, seller, &L.out[opt], L.hedge ? &L.hedge[2 * opt + (seller ? 0 : 1)] : nullptr,
+                err |= tc_root(mine, oc, seller, &L.out[opt], L.hedge ? &L.hedge[2 * opt + (seller ? 0 : 1)] : nullptr,
                                   lane);
             }
         }
@@ -737,6 +704,15 @@ static StripCaps strip_caps_light(int N) {
     c.hscr_cap = 0;
     c.zbuf_cap = 0;
     return c;
+}
+
+void strip_tc_caps(int N, int level, int& rarena, int& carena, int& hscr, int& zbuf, int& tl) {
+    const StripCaps c = strip_caps(N, level);
+    rarena = c.rarena_cap;
+    carena = c.carena_cap;
+    hscr = c.hscr_cap;
+    zbuf = c.zbuf_cap;
+    tl = c.TL;
 }
 
 size_t strip_ws_bytes_per_warp(int N, int level) { return strip_layout(N, strip_caps(N, level)).total; }
