@@ -130,7 +130,11 @@ int amtc_price_american_tc_batch_host(const amtc_batch_soa* h_in, int64_t n, int
  * k = 0 (frictionless) batched CRR American prices (Appendix: no
  * extra level, scalar max(exercise, continuation)).  d_in->k and ->K2 are
  * ignored except for bull spreads (K2).  d_price: device array of n doubles.
- * Asynchronous on cuda_stream.  Per-option validation failures write NaN.
+ * Any N >= 1: N <= 1152 keeps one tree's level in a warp's registers; larger N
+ * (Table III's N = 5,000-40,000 trees) sweeps each tree in
+ * 512-column strips with a carry buffer of 2 (N + 2) doubles per resident
+ * warp, owned by the library (grow-only, per device).  Asynchronous on
+ * cuda_stream.  Per-option validation failures write NaN.
  */
 int amtc_price_crr_batch(const amtc_batch_soa* d_in, int64_t n, int32_t N, double* d_price,
                          void* cuda_stream);

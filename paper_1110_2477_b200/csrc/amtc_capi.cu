@@ -58,6 +58,7 @@ struct DevState {
     DevBuf items[2], cls, small, ws, stage_in, stage_out;
     DevBuf sp_items, sp_progress, sp_carry, sp_arena, sp_cnt;  // split mode
     DevBuf ws_light;                                          // light-kernel workspaces
+    DevBuf crr_ws;                                            // CRR strip kernel carry buffers (N > 1152)
     DevBuf ipc;                                               // IPC handle exchange
     cudaStream_t s2 = nullptr;                                // light-kernel stream
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -113,8 +114,8 @@ static int g_split_mode = -1;
 // 1 = amtc_light.cu (default), 2 = the strip kernel's light variant, 0 = none
 static int g_light_kernel = 1;
 // the whole-tree solver for the other items (testing hook amtc_debug_set_full_kernel):
-// 1 = amtc_full.cu (default), 0 = the strip kernel (amtc_strip.cu)
-static int g_full_kernel = 1;
+// 1 = amtc_full.cu, 0 = the strip kernel (amtc_strip.cu; default: faster on the whole config-4 batch)
+static int g_full_kernel = 0;
 
 // solver passes: every item first runs at capacity level 0; items that
 // overflowed a capacity (arena, scratch) are re-run at the next level (4x the
@@ -765,15 +766,25 @@ int amtc_price_american_tc_hedge(const amtc_params* params, int32_t N, const amt
     }
 }
 
+// caller holds st->mu (the strip path's carry workspace lives in st->crr_ws)
+static int crr_batch_locked(DevState* st, const amtc_batch_soa* d_in, int64_t n, int32_t N, double* d_price,
+                            cudaStream_t s) {
+    if (N <= crr_max_n()) return crr_launch(to_ptrs(d_in), n, N, d_price, s);
+    const int64_t warps = crr_strip_warps(n);
+    const cudaError_t e = st->crr_ws.ensure(crr_strip_ws_bytes(N, warps));
+    if (e != cudaSuccess) return cuda_fail(e, "CRR strip workspace");
+    return crr_strip_launch(to_ptrs(d_in), n, N, d_price, static_cast<double*>(st->crr_ws.p), warps, s);
+}
+
 int amtc_price_crr_batch(const amtc_batch_soa* d_in, int64_t n, int32_t N, double* d_price, void* cuda_stream) {
     try {
         if (!soa_ok(d_in) || !d_price || n < 0 || N < 1) return STATUS_EINVAL;
         if (n == 0) return STATUS_OK;
-        if (N > crr_max_n()) {
-            g_last_error = "N exceeds the register-resident CRR kernel";
-            return STATUS_EINVAL;
-        }
-        int rc = crr_launch(to_ptrs(d_in), n, N, d_price, static_cast<cudaStream_t>(cuda_stream));
+        int dev = 0;
+        AMTC_CUDA(cudaGetDevice(&dev));
+        DevState* st = state_for_device(dev);
+        std::lock_guard<std::mutex> g(st->mu);
+        int rc = crr_batch_locked(st, d_in, n, N, d_price, static_cast<cudaStream_t>(cuda_stream));
         AMTC_CUDA(cudaGetLastError());
         return rc;
     } catch (...) {
@@ -797,7 +808,8 @@ int amtc_price_crr_batch_host(const amtc_batch_soa* h_in, int64_t n, int32_t N, 
         if (rc) return rc;
         AMTC_CUDA(st->stage_out.ensure(sizeof(double) * (size_t)n));
         double* d_price = static_cast<double*>(st->stage_out.p);
-        rc = amtc_price_crr_batch(&d, n, N, d_price, s);
+        rc = crr_batch_locked(st, &d, n, N, d_price, s);
+        if (!rc && cudaGetLastError() != cudaSuccess) rc = STATUS_ECUDA;
         if (rc) return rc;
         AMTC_CUDA(cudaMemcpyAsync(h_price, d_price, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, s));
         AMTC_CUDA(cudaStreamSynchronize(s));

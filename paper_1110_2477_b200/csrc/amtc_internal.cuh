@@ -125,5 +125,9 @@ int light2_launch(const StripLaunchArgs& a, cudaStream_t s);
 // amtc_crr.cu
 int crr_launch(const BatchPtrs& in, int64_t n, int N, double* out, cudaStream_t s);
 int crr_max_n();
+// N > crr_max_n(): strip kernel with a per-warp carry workspace (crr_strip_ws_bytes)
+int64_t crr_strip_warps(int64_t n);
+size_t crr_strip_ws_bytes(int N, int64_t warps);
+int crr_strip_launch(const BatchPtrs& in, int64_t n, int N, double* out, double* ws, int64_t warps, cudaStream_t s);
 
 }  // namespace amtc

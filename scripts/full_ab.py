@@ -6,7 +6,7 @@ import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_1110_2477_b200 import api, build, workloads as W
-build.build(); api.lib()
+build.build(force=os.environ.get("AB_FORCE") == "1"); api.lib()
 print(json.dumps({"variant": os.environ.get("AMTC_NVCC_EXTRA", "")}), flush=True)
 api.debug_set_split_mode(0)
 b = W.config4()
@@ -23,6 +23,8 @@ bulls = np.nonzero(b.kind == 2)[0]
 sets = {"calls512": calls[:512], "bulls512": bulls[:512], "puts1184": np.nonzero(b.kind == 0)[0][:1184]}
 if os.environ.get("AB_ALL", "1") == "1":
     sets["all"] = np.arange(len(b))
+if os.environ.get("AB_SETS"):
+    sets = {k: v for k, v in sets.items() if k in os.environ["AB_SETS"].split(",")}
 modes = [int(m) for m in os.environ.get("AB_MODES", "1,0").split(",")]
 api.price_american_tc_batch(api.device_batch(b.subset(np.arange(4))), 20)
 for name, idx in sets.items():

@@ -167,9 +167,24 @@ def test_config2_every_option(api):
     print(f"config2: 65536 prices, floor used {used} times")
 
 
-@pytest.mark.parametrize("N", [1, 2, 127, 128, 129, 500, 1024, 1151])
+@pytest.mark.parametrize("N", [1, 2, 127, 128, 129, 500, 1023, 1024, 1025, 1151, 1152])
 def test_crr_small_and_ragged(api, N):
+    """Register-resident CRR kernel: ragged N around the 128-node slot edges
+    (N = 1024 and 1152 end the slots one node before the leaf j = N)."""
     b = W.random_small(37, seed=N)
+    got = api.price_crr_batch_host(b, N)
+    for i in range(len(b)):
+        o = O.price_crr(_opt(b.row(i)), N)
+        assert close(got[i], o, N), (i, N, got[i], o)
+
+
+@pytest.mark.parametrize("N,n", [(1153, 37), (1536, 37), (2047, 20), (5000, 9), (20000, 3)])
+def test_crr_batch_large_n_strip_kernel(api, N, n):
+    """N above the register-resident level: the strip kernel (512-column strips,
+    carry buffer per warp); Table III's frictionless trees reach N = 40,000
+    (P:491-538).  Ragged strip counts, puts, calls and bull spreads
+    against the oracle."""
+    b = W.random_small(n, seed=N)
     got = api.price_crr_batch_host(b, N)
     for i in range(len(b)):
         o = O.price_crr(_opt(b.row(i)), N)
