@@ -150,7 +150,7 @@ def debug_set_light_kernel(on: bool) -> None:
 
 
 def debug_set_full_kernel(which: int) -> None:
-    """Testing hook: 1 the full solver of amtc_full.cu (default), 0 the strip kernel."""
+    """Testing hook: 1 the full solver of amtc_full.cu, 0 the strip kernel (default)."""
     lib().amtc_debug_set_full_kernel(int(which))
 
 

@@ -54,4 +54,4 @@ for name, idx in sets.items():
         dd = max(np.nanmax(np.abs(res[modes[0]]["ask"] - res[modes[1]]["ask"])),
                  np.nanmax(np.abs(res[modes[0]]["bid"] - res[modes[1]]["bid"])))
         print(json.dumps({"set": name, "max_abs_diff_modes": float(dd)}), flush=True)
-api.debug_set_full_kernel(1)
+api.debug_set_full_kernel(0)
