@@ -401,8 +401,11 @@ def run_amtc(args):
     roofline = None
     if args.config == 4:
         if z is not None:
-            seller_light = np.isin(b.kind[idx], [0, 1])             # seller of a put / call: light kernel
-            buyer_light = b.kind[idx] == 0                           # buyer of a put: light kernel
+            # the prepare kernel's item classes (amtc_prepare.cu item_class): the light
+            # kernel takes put sellers, call sellers with k/h < 4 and put buyers
+            kh = b.k[idx] / (b.sigma[idx] * np.sqrt(b.T[idx] / N))
+            seller_light = (b.kind[idx] == 0) | ((b.kind[idx] == 1) & (kh < 4.0))
+            buyer_light = b.kind[idx] == 0
             ops_a = z["fp64_ops_ask"][idx].astype(np.float64)
             ops_b = z["fp64_ops_bid"][idx].astype(np.float64)
             light_ops = ops_a[seller_light].sum() + ops_b[buyer_light].sum()

@@ -280,12 +280,18 @@ void amtc_debug_set_light_kernel(int on);
 
 /* TESTING HOOK: which kernel runs the whole-tree items that may grow heavy
    node functions (buyers of calls / bull spreads, bull-spread sellers, and
-   every item when the light kernel is off): 1 (default) the full solver of
+   every item when the light kernel is off): 0 (default; measured faster on
+   the whole config-4 batch) the strip kernel of amtc_strip.cu, also the
+   split-mode and sharded-tree kernel; any other value the full solver of
    amtc_full.cu (strip matrix in shared memory, row / carry arenas, tier-3
-   CTA work sharing); 0 the strip kernel of amtc_strip.cu (the round-1
-   solver, still the split-mode and sharded-tree kernel).  Any other value
-   restores the default. */
+   CTA work sharing). */
 void amtc_debug_set_full_kernel(int which);
+
+/* TESTING HOOK: split mode (few trees, strips pipelined over warps) runs
+   batches whose items are all light (sellers of puts / calls, put buyers) on
+   the light kernel's split variant (carry hand-off staged one level ahead);
+   on = 0 sends them to the strip kernel's split mode instead.  Default 1. */
+void amtc_debug_set_light_split(int on);
 
 /* DEVELOPER HOOK: the full solver's clock64 phase accumulators (summed over
    warps since the last reset; out: 8 uint64, HOST): [0] cycles inside heavy

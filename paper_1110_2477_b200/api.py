@@ -59,7 +59,7 @@ EXPORTS = ["amtc_price_american_tc", "amtc_price_american_tc_batch", "amtc_price
            "amtc_price_crr_batch", "amtc_price_crr_batch_host", "amtc_strerror", "amtc_last_error",
            "amtc_launch_count", "amtc_tc_last_stats", "amtc_debug_set_heavy_threshold",
            "amtc_price_crr_tree", "amtc_comm_unique_id", "amtc_comm_init", "amtc_comm_destroy",
-           "amtc_price_tree_sharded", "amtc_debug_set_split_mode", "amtc_debug_set_light_kernel", "amtc_debug_set_full_kernel", "amtc_debug_full_profile",
+           "amtc_price_tree_sharded", "amtc_debug_set_split_mode", "amtc_debug_set_light_kernel", "amtc_debug_set_full_kernel", "amtc_debug_set_light_split", "amtc_debug_full_profile",
            "amtc_debug_set_arena_shift", "amtc_tree_shard_plan", "amtc_price_american_tc_hedge",
            "amtc_batch_shard_plan", "amtc_tree_band_plan"]
 
@@ -108,6 +108,8 @@ def lib():
         L.amtc_debug_full_profile.argtypes = [C.c_void_p, C.c_int]
         L.amtc_debug_set_full_kernel.restype = None
         L.amtc_debug_set_full_kernel.argtypes = [C.c_int]
+        L.amtc_debug_set_light_split.restype = None
+        L.amtc_debug_set_light_split.argtypes = [C.c_int]
         L.amtc_debug_set_light_kernel.restype = None
         L.amtc_debug_set_light_kernel.argtypes = [C.c_int]
         L.amtc_debug_set_split_mode.restype = None
@@ -152,6 +154,11 @@ def debug_set_light_kernel(on: bool) -> None:
 def debug_set_full_kernel(which: int) -> None:
     """Testing hook: 1 the full solver of amtc_full.cu, 0 the strip kernel (default)."""
     lib().amtc_debug_set_full_kernel(int(which))
+
+
+def debug_set_light_split(on: bool) -> None:
+    """Testing hook: split mode of the light kernel for batches of light trees (default on)."""
+    lib().amtc_debug_set_light_split(int(on))
 
 
 def debug_full_profile(reset: bool = True):

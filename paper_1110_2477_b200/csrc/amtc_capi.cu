@@ -116,6 +116,8 @@ static int g_light_kernel = 1;
 // the whole-tree solver for the other items (testing hook amtc_debug_set_full_kernel):
 // 1 = amtc_full.cu, 0 = the strip kernel (amtc_strip.cu; default: faster on the whole config-4 batch)
 static int g_full_kernel = 0;
+// split mode of the light kernel for batches of light trees (testing hook amtc_debug_set_light_split)
+static int g_light_split = 1;
 
 // solver passes: every item first runs at capacity level 0; items that
 // overflowed a capacity (arena, scratch) are re-run at the next level (4x the
@@ -195,6 +197,73 @@ static int tc_batch_device(const amtc_batch_soa* d_in, int64_t n, int32_t N, amt
         const int64_t nsp = n2 * S;
         bool want = (g_split_mode == 1 || (g_split_mode < 0 && n2 <= warps_total / 4)) && N >= 64 &&
                     nsp < ((int64_t)1 << 30);
+        // every queued item light (sellers of puts / calls, put buyers: class 0)?
+        // then the light kernel's split mode (prefetched hand-off, one level ahead)
+        if (want && g_light_kernel == 1 && g_light_split && st->light2_occupancy > 0) {
+            int h1 = -1;
+            AMTC_CUDA(cudaMemcpyAsync(&h1, small + SM_HIST + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+            AMTC_CUDA(cudaStreamSynchronize(s));
+            const size_t lcarry = light2_split_carry_bytes(N);
+            const size_t lneed = (size_t)nsp * (lcarry + sizeof(int));
+            if (h1 == 0 && lneed <= budget / 2) {
+                const size_t wsl = light2_ws_bytes_per_warp(N);
+                const int lw = light2_warps_per_cta();
+                // every CTA slot of the device, not just enough for the items: strips are
+                // claimed first-come, so they spread over all SMs (a strip pipeline is
+                // latency bound; packing 8 strips per SM triples the per-level time)
+                int64_t ctas = (int64_t)st->sm_count * st->light2_occupancy;
+                ctas = std::min<int64_t>(ctas, (int64_t)((budget - lneed) / (wsl * lw)));
+                if (ctas >= 1) {
+                    AMTC_CUDA(st->ws_light.ensure(wsl * lw * (size_t)ctas));
+                    AMTC_CUDA(st->items[1].ensure(sizeof(int) * (size_t)std::max<int64_t>(n2, nsp)));
+                    AMTC_CUDA(st->sp_items.ensure(sizeof(int) * (size_t)nsp));
+                    AMTC_CUDA(st->sp_progress.ensure(sizeof(int) * (size_t)nsp));
+                    AMTC_CUDA(st->sp_carry.ensure(lcarry * (size_t)nsp));
+                    AMTC_CUDA(cudaMemsetAsync(st->sp_progress.p, 0x7f, sizeof(int) * (size_t)nsp, s));
+                    tc_launch_split_expand(q_items, q_count, S, nsp, static_cast<int*>(st->sp_items.p),
+                                           small + SM_SPLITN, s);
+                    AMTC_CUDA(cudaMemsetAsync(small + SM_WORK, 0, sizeof(int), s));
+                    AMTC_CUDA(cudaMemsetAsync(small + SM_OVF0, 0, sizeof(int), s));
+                    AMTC_CUDA(cudaEventRecord(st->ev[0], s));
+                    AMTC_CUDA(cudaEventRecord(st->kev[2], s));
+                    StripLaunchArgs A;
+                    A.in = in;
+                    A.N = N;
+                    A.out = out;
+                    A.items = static_cast<int*>(st->sp_items.p);
+                    A.n_items = small + SM_SPLITN;
+                    A.work_counter = small + SM_WORK;
+                    A.ovf_items = static_cast<int*>(st->items[1].p);
+                    A.ovf_count = small + SM_OVF0;
+                    A.vertex_sum = reinterpret_cast<unsigned long long*>(small + SM_VSUM);
+                    A.ws = static_cast<char*>(st->ws_light.p);
+                    A.ws_stride = wsl;
+                    A.level = 0;
+                    A.ctas = (int)ctas;
+                    A.split_S = S;
+                    A.progress = static_cast<int*>(st->sp_progress.p);
+                    A.carry = static_cast<char*>(st->sp_carry.p);
+                    A.carry_stride = lcarry;
+                    A.hedge = d_hedge;
+                    if (light2_launch(A, s) != STATUS_OK) return cuda_fail(cudaGetLastError(), "light_kernel launch");
+                    AMTC_CUDA(cudaEventRecord(st->kev[3], s));
+                    AMTC_CUDA(cudaEventRecord(st->ev[1], s));
+                    passes = 1;
+                    light_ran = true;
+                    AMTC_CUDA(cudaMemcpyAsync(&ovf_host, small + SM_OVF0, sizeof(int), cudaMemcpyDeviceToHost, s));
+                    AMTC_CUDA(cudaStreamSynchronize(s));
+                    if (ovf_host == 0) goto finish;
+                    // a strip outgrew the light kernel: redo every tree on the general split / whole-tree path
+                    st->retried = ovf_host;
+                    tc_launch_prepare(in, n, N, out, static_cast<unsigned char*>(st->cls.p), small + SM_HIST,
+                                      static_cast<int*>(st->items[0].p), s);
+                    AMTC_CUDA(cudaMemsetAsync(small + SM_VSUM, 0, sizeof(unsigned long long), s));
+                    ovf_host = 0;
+                    passes = 0;
+                    light_ran = false;
+                }
+            }
+        }
         const size_t carry_b = strip_carry_bytes(N);
         const int acap = strip_split_arena_cap(N);
         const size_t need_b = (size_t)nsp * (carry_b + 2 * sizeof(int)) + (size_t)n2 * acap * strip_vtx_bytes();
@@ -883,6 +952,8 @@ int amtc_debug_full_profile(uint64_t out[8], int reset) {
     return full_profile(reinterpret_cast<unsigned long long*>(out), reset);
 }
 void amtc_debug_set_full_kernel(int which) { g_full_kernel = (which == 0) ? 0 : 1; }
+
+void amtc_debug_set_light_split(int on) { g_light_split = on ? 1 : 0; }
 void amtc_debug_set_light_kernel(int on) { g_light_kernel = (on >= 0 && on <= 2) ? on : 1; }
 
 void amtc_debug_set_arena_shift(int shift) { strip_set_arena_shift(shift); }

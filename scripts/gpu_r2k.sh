@@ -10,6 +10,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 600 python scripts/parity_hist.py > gpurun_out/parity_$T.log 2>&1; echo parity rc=$?; tail -c 1500 gpurun_out/parity_$T.log
 cp profiles/r02_parity_error_hist.json gpurun_out/ 2>/dev/null
 timeout 900 python bench.py > gpurun_out/bench_$T.log 2>&1; echo bench rc=$?; tail -c 4000 gpurun_out/bench_$T.log
+for c in 2 5 3 1; do timeout 600 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/bench_c${c}_$T.log 2>&1; echo bench$c rc=$?; done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$T.csv \
    python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch_$T.log 2>&1; echo ncu-launches rc=$?
 timeout 2400 ncu --set full --clock-control none -k regex:"strip_kernel|light_kernel" -s 2 -c 2 -o gpurun_out/${T}_full_step \

@@ -255,6 +255,28 @@ def test_split_mode_matches_oracle(api, N):
     np.testing.assert_allclose(got["bid"], ref["bid"], rtol=1e-12, atol=floor(N))
 
 
+@pytest.mark.parametrize("N", [64, 95, 97, 300])
+@pytest.mark.parametrize("light_split", [1, 0])
+def test_split_mode_light_trees(api, N, light_split):
+    """A batch of light trees only (puts: both parties' functions stay within the
+    light kernel's 6-vertex slots) in split mode: by default on the light
+    kernel's split variant (carry records staged one level ahead through
+    per-(tree, strip) columns and progress counters), else on the strip
+    kernel's split mode; both against the oracle, ragged last strips
+    included (N = 95, 97)."""
+    b = W.random_small(40, seed=5100 + N, k_max=0.05)
+    b = b.subset(np.nonzero(b.kind == W.PUT)[0][:8])
+    try:
+        api.debug_set_split_mode(1)
+        api.debug_set_light_split(light_split)
+        got, rc = api.price_american_tc_batch_host(b, N)
+    finally:
+        api.debug_set_split_mode(-1)
+        api.debug_set_light_split(1)
+    assert rc == 0
+    assert_quotes(got, b, N)
+
+
 def test_config5b_single_tree_split(api):
     """BASELINE config 5b shape at a size the oracle finishes quickly (N=1200),
     through the north-star single-option call (automatic split mode)."""

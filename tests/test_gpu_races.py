@@ -103,6 +103,17 @@ def test_split_mode_progress_handoff_deterministic(api, batch, tl):
     _oracle_sample(api, sub, runs[0], n=len(sub))
 
 
+def test_light_split_handoff_deterministic(api, batch):
+    """The light kernel's split mode (light trees only: puts): cp.async-staged
+    carry records behind HBM progress counters, bitwise equal over runs."""
+    api.debug_set_split_mode(1)
+    api.debug_set_heavy_threshold(-1)
+    sub = batch.subset(np.nonzero(batch.kind == W.PUT)[0][::15])
+    runs = _runs(api, api.device_batch(sub), reps=4)
+    _bitwise_equal(runs)
+    _oracle_sample(api, sub, runs[0], n=len(sub))
+
+
 def test_modes_agree_within_tolerance(api, batch):
     """The same batch through whole-tree mode (both full kernels) and split
     mode: equal within the parity tolerance (different tiers may round
