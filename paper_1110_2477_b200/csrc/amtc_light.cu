@@ -238,9 +238,31 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) light_kernel(const __grid_co
             const bool has_right = s < N / 32;
             const int t_end = max(j0, 1);
             int seen = INT_MAX;  // split mode: lowest level of strip s+1 known to be published
+            bool staged_next = false;  // the record of the next level's down child is already in flight
             for (int t = N; t >= t_end; --t) {
-                // the carry record of level t+1 (lane 31's down child now), staged by the
-                // cp.async issued during level t+1, goes into column 32 + ((t+1) & 1)
+                // the carry record of level t+1 (lane 31's down child now), staged by a
+                // cp.async, goes into column 32 + ((t+1) & 1).  Whole-tree mode staged it
+                // during level t+1; split mode did so only if strip s+1 had published it
+                // by then, else it waits for it here (the record is needed now)
+                if (SPLIT && !staged_next && t < N && has_right && t + 1 >= j0 + 32) {
+                    if (seen > t + 1) {
+                        int pv = 0;
+                        if (lane == 0) {
+                            int spins = 0;  // the producer is usually a level away: spin, then back off
+                            while ((pv = *prog_in) > t + 1) {
+                                if (++spins > 32) __nanosleep(64);
+                            }
+                        }
+                        seen = __shfl_sync(LFULL, pv, 0);
+                        if (seen < 0) {  // strip s+1 failed: finish, the tree is re-run
+                            err |= DEV_OVERFLOW;
+                            seen = INT_MIN;
+                        }
+                        __threadfence();
+                    }
+                    if (lane < (2 + 3 * C) / 2)
+                        cp_async16(&S.stg[(t + 1) & 1][2 * lane], &cin[t + 1].d[2 * lane]);
+                }
                 cp_async_wait_all();
                 __syncwarp();
                 if (t < N && has_right && t + 1 >= j0 + 32 && lane < 2 + 3 * C) {
@@ -253,29 +275,28 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) light_kernel(const __grid_co
                         (&S.row[(q / 3) * LW + 32 + par].x)[q % 3] = v;
                     }
                 }
-                // stage the record of level t (lane 31's down child at level t-1); in
-                // split mode first wait until strip s+1 has published level t
+                // stage the record of level t (lane 31's down child at level t-1) while
+                // level t is computed; split mode only if strip s+1 has published it
+                // already (one non-blocking look at its progress), so the node updates
+                // of level t never wait for the strip to the right
+                staged_next = false;
                 if (has_right && t >= j0 + 32) {
-                    // poll only when the last published level seen is above t (the
-                    // producer publishes every AMTC_L2_PUB levels and is usually ahead)
+                    bool ready = true;
                     if (SPLIT && seen > t) {
                         int pv = 0;
-                        if (lane == 0) {
-                            int spins = 0;  // the producer is usually a level away: spin, then back off
-                            while ((pv = *prog_in) > t) {
-                                if (++spins > 32) __nanosleep(64);
-                            }
+                        if (lane == 0) pv = *prog_in;
+                        pv = __shfl_sync(LFULL, pv, 0);
+                        if (pv < seen) {
+                            seen = pv < 0 ? INT_MIN : pv;
+                            if (pv < 0) err |= DEV_OVERFLOW;
+                            __threadfence();
                         }
-                        seen = __shfl_sync(LFULL, pv, 0);
-                        if (seen < 0) {  // strip s+1 failed: finish, the tree is re-run
-                            err |= DEV_OVERFLOW;
-                            seen = INT_MIN;
-                        }
-#ifndef AMTC_DIAG_NO_CFENCE
-                        __threadfence();
-#endif
+                        ready = seen <= t;
                     }
-                    if (lane < (2 + 3 * C) / 2) cp_async16(&S.stg[t & 1][2 * lane], &cin[t].d[2 * lane]);
+                    if (ready) {
+                        if (lane < (2 + 3 * C) / 2) cp_async16(&S.stg[t & 1][2 * lane], &cin[t].d[2 * lane]);
+                        staged_next = true;
+                    }
                 }
                 __syncwarp();
                 const bool active = j <= t;
@@ -349,9 +370,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) light_kernel(const __grid_co
                         rec[lane] = (&S.row[(q / 3) * LW].x)[q % 3];
                     }
                     if (SPLIT && (t % AMTC_L2_PUB == 0 || t == t_end)) {  // publish levels >= t to strip s-1
-#ifndef AMTC_DIAG_NO_PFENCE
                         __threadfence();
-#endif
                         __syncwarp();
                         if (lane == 0) *prog_out = t;
                     }

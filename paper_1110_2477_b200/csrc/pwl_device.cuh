@@ -41,7 +41,10 @@ enum : int { DEV_OK = 0, DEV_OVERFLOW = 1, DEV_UNBOUNDED = 2 };
 //    not "cross" another it merely touches (ties are broken by slope);
 //  * a piece shorter than TOL_X (1 + |x|) is folded into its neighbour.
 constexpr double TOL_F = 1e-14;
-constexpr double TOL_X = 1e-14;
+#ifndef AMTC_TOL_X
+#define AMTC_TOL_X 1e-13
+#endif
+constexpr double TOL_X = AMTC_TOL_X;
 AMTC_HD double ftol(double a, double b) { return TOL_F * (fabs(a) + fabs(b) + 1.0); }
 AMTC_HD double xtol(double x) { return TOL_X * (1.0 + fabs(x)); }
 

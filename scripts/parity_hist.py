@@ -62,7 +62,7 @@ def main():
     p = api.price_crr_batch(api.device_batch(b2), W.CONFIG2_N)
     torch.cuda.synchronize()
     out["config2"] = {"N": W.CONFIG2_N, "price": hist(p.cpu().numpy(), z2["price"], W.CONFIG2_N, b2.S0)}
-    path = os.path.join(ROOT, "profiles", "r02_parity_error_hist.json")
+    path = os.environ.get("PH_OUT") or os.path.join(ROOT, "profiles", "r02_parity_error_hist.json")
     json.dump(out, open(path, "w"), indent=1)
     print(json.dumps({k: (v if k not in ("config4", "config2") else
                           {p_: {kk: vv for kk, vv in v[p_].items() if kk in ("n", "pass", "floor_used",
