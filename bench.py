@@ -426,6 +426,29 @@ def run_amtc(args):
                                        "scaling 2) per option and party, tests/golden/oracle_config4_full.npz",
                         "peak_source": peak_src + "; DFMA = 1 instruction (the cost model counts instructions)",
                         "flop_peak_tflops": flop_peak / 1e12}
+            # the committed ncu launch list of this command (serialised, cold cache): each
+            # kernel's share of the step, to compare with the live event times above
+            lf = os.path.join(ROOT, "profiles", "r02_launches_config4.csv")
+            if os.path.exists(lf):
+                try:
+                    import csv as _csv
+                    rows = [r for r in _csv.reader(open(lf)) if len(r) > 10]
+                    ki, vi = rows[0].index("Kernel Name"), rows[0].index("Metric Value")
+                    tot, per = 0.0, {}
+                    for r in rows[1:]:
+                        ns = float(r[vi].replace(",", ""))
+                        tot += ns
+                        key = "full" if "strip_kernel" in r[ki] or "full_kernel" in r[ki] else (
+                            "light" if "light_kernel" in r[ki] else "other")
+                        per[key] = per.get(key, 0.0) + ns
+                    roofline["launch_list"] = {k: {"share": v / tot, "ns_total": v} for k, v in per.items()}
+                    roofline["launch_list_source"] = "profiles/r02_launches_config4.csv (ncu gpu__time_duration.sum, serialised)"
+                except Exception:
+                    pass
+            if "light" in per_k:
+                per_k["light"]["note"] = ("event span on the second stream: includes the wait for SMs the full kernel "
+                                          "holds (its CTAs take ~210 KB of shared memory), so it overstates the light "
+                                          "kernel's run time; the launch list's serialised time is the kernel's own")
             tf = os.path.join(ROOT, "profiles", "r02_traffic_config4.json")
             if os.path.exists(tf):
                 try:

@@ -427,6 +427,21 @@ __device__ __forceinline__ double excl_prefix_min(double v, int lane) {
     const double px = __shfl_up_sync(FULLM, x, 1);
     return lane > 0 ? px : INFINITY;
 }
+// exclusive prefix sum of small non-negative counts (v < 2^B) by bit planes:
+// B independent ballots instead of a 5-deep shuffle chain
+template <int B>
+__device__ __forceinline__ int excl_prefix_sum_bits(int v, int lane, int& total) {
+    const unsigned lt = (1u << lane) - 1u;
+    int off = 0, tot = 0;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+        const unsigned m = __ballot_sync(FULLM, (v >> b) & 1);
+        off += __popc(m & lt) << b;
+        tot += __popc(m) << b;
+    }
+    total = tot;
+    return off;
+}
 __device__ __forceinline__ int excl_prefix_sum(int v, int lane, int& total) {
     int x = v;
 #pragma unroll
@@ -1075,11 +1090,15 @@ static __device__ __noinline__ int node_update_block(const Fn U, const Fn D, dou
         if (lane == 0) { x_prev = cx; wRp = cwr; }
         const WV3 w = w_vertices(e, valid, x_prev, wRp, k0 + lane == h.klast, h.wInf_U);
         int tot;
-        const int off = excl_prefix_sum(w.n, lane, tot);
+        const int off = excl_prefix_sum_bits<2>(w.n, lane, tot);  // w.n <= 3
         if (nW + tot > wcap) return DEV_FALLBACK;  // cannot happen
-        for (int q = 0; q < w.n; ++q) {
-            const WV v = w.get(q);
-            Wb[nW + off + q] = Vtx{v.x, v.f, v.sR};
+        // compile-time q: w stays in registers (a runtime index put it in local memory)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            if (q < w.n) {
+                const WV v = w.get(q);
+                Wb[nW + off + q] = Vtx{v.x, v.f, v.sR};
+            }
         }
         nW += tot;
         const unsigned bu = __ballot_sync(FULLM, valid && (code & 1));
@@ -1236,7 +1255,8 @@ static __device__ __noinline__ int node_update_block(const Fn U, const Fn D, dou
         const int drop_first = (fold && (pl >= 0 || total > 0)) ? 1 : 0;
         cnt -= drop_first;
         int tot;
-        const int off = excl_prefix_sum(cnt, lane, tot);
+        static_assert(STAGE < 64, "cnt < 2^6");
+        const int off = excl_prefix_sum_bits<6>(cnt, lane, tot);  // 0 <= cnt <= STAGE
         if (base + total + tot > acap) { err = DEV_OVERFLOW; break; }
         for (int q = 0; q < cnt; ++q)
             arena[base + total + off + q] = st.at(q + skip0 + drop_first);
@@ -1276,7 +1296,9 @@ static __device__ __noinline__ double root_min(const Fn U, const Fn D, double lo
     double fx = INFINITY, fval = 0.0;       // the first vertex (W(0) from the left tail if none <= 0)
     for (int blk = 0; blk < nb; ++blk) {
         const BlockW B = block_w(h, blk, lane);
-        for (int q = 0; q < B.w.n; ++q) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            if (q >= B.w.n) break;
             const WV w = B.w.get(q);
             if (w.x >= 0.0) {
                 const double g = fma(-lo, w.x, w.f);

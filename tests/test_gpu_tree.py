@@ -1,6 +1,7 @@
 """GPU parity of the single large-tree path (config 5a) and of the sharded
 entry point on one rank, through the C-ABI, against the CPU oracle."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -104,3 +105,17 @@ def test_very_long_tree_1e6(api):
     g6 = api.price_crr_tree(a["S0"], a["K"], a["T"], a["sigma"], a["R"], 1_000_000, O.PUT)
     g4 = api.price_crr_tree(a["S0"], a["K"], a["T"], a["sigma"], a["R"], 40_000, O.PUT)
     assert abs(g6 - 13.906) <= 5e-4 and abs(g6 - g4) <= 5e-4, (g6, g4)
+
+
+@pytest.mark.parametrize("N", [200_000, 400_000])
+def test_long_tree_against_oracle_golden(api, N):
+    """SURVEY 8(f) NEXT #4 backed by the oracle beyond the suite's own reach: the
+    appendix put at N = 2e5 and 4e5 against oracle values cached by
+    scripts/make_tree_refs.py (plain scalar CRR, ~12 / 48 CPU-minutes each)."""
+    import json
+    path = os.path.join(os.path.dirname(__file__), "golden", f"oracle_tree_appendix_put_N{N}.json")
+    ref = json.load(open(path))
+    a = W.appendix_put().row(0)
+    assert (ref["S0"], ref["K"], ref["T"], ref["sigma"], ref["R"]) == (a["S0"], a["K"], a["T"], a["sigma"], a["R"])
+    g = api.price_crr_tree(a["S0"], a["K"], a["T"], a["sigma"], a["R"], N, O.PUT)
+    assert _close(g, ref["price"], N), (g, ref["price"])
