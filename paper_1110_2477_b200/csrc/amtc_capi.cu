@@ -949,7 +949,10 @@ void amtc_debug_set_heavy_threshold(int tl) { strip_set_heavy_threshold(tl); }
 void amtc_debug_set_split_mode(int mode) { g_split_mode = mode < 0 ? -1 : (mode ? 1 : 0); }
 
 int amtc_debug_full_profile(uint64_t out[8], int reset) {
-    return full_profile(reinterpret_cast<unsigned long long*>(out), reset);
+    // the full solver's counters (-DAMTC_F_PROF=1), else the light kernel's split-mode ones (-DAMTC_L2_PROF=1)
+    const int rc = full_profile(reinterpret_cast<unsigned long long*>(out), reset);
+    if (rc == STATUS_OK) return rc;
+    return light_profile(reinterpret_cast<unsigned long long*>(out), reset);
 }
 void amtc_debug_set_full_kernel(int which) { g_full_kernel = (which == 0) ? 0 : 1; }
 

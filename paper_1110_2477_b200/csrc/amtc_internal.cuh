@@ -121,7 +121,8 @@ size_t light2_ws_bytes_per_warp(int N);
 int light2_warps_per_cta();
 int light2_ctas_per_sm();
 int light2_launch(const StripLaunchArgs& a, cudaStream_t s);
-size_t light2_split_carry_bytes(int N);  // one (tree, strip) carry column of the light kernel's split mode
+size_t light2_split_carry_bytes(int N);
+int light_profile(unsigned long long out[8], int reset);  // -DAMTC_L2_PROF=1 developer counters  // one (tree, strip) carry column of the light kernel's split mode
 
 // amtc_crr.cu
 int crr_launch(const BatchPtrs& in, int64_t n, int N, double* out, cudaStream_t s);

@@ -55,7 +55,7 @@ namespace amtc {
 #define AMTC_L2_B 10
 #endif
 #ifndef AMTC_L2_WARPS
-#define AMTC_L2_WARPS 8
+#define AMTC_L2_WARPS 6  // 12 warps / SM at 168 registers: whole config-4 batch 9.24 -> 9.02 s (8 warps, 128 regs)
 #endif
 #ifndef AMTC_L2_MINB
 #define AMTC_L2_MINB 2
@@ -105,6 +105,15 @@ struct LightSmem {
 
 template <class T>
 __device__ __forceinline__ T vld(const T& x) { return *(const volatile T*)&x; }
+
+// developer instrumentation (-DAMTC_L2_PROF=1, split mode): per-warp clock64
+// accumulators summed into g_lprof, read through amtc_debug_full_profile:
+// [0] cycles in the level loop, [1] cycles in blocking waits for the strip to
+// the right, [2] blocking waits, [3] levels, [4] records staged early
+#ifndef AMTC_L2_PROF
+#define AMTC_L2_PROF 0
+#endif
+__device__ unsigned long long g_lprof[8];
 
 // one double global -> shared without a register (cp.async, L1-bypassing 8-byte copy)
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
@@ -237,6 +246,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) light_kernel(const __grid_co
             double disc = exp(-oc.rho * (double)N);
             const bool has_right = s < N / 32;
             const int t_end = max(j0, 1);
+#if AMTC_L2_PROF
+            long long pw = 0, nw = 0, ne = 0;
+            const long long p0 = clock64();
+#endif
             int seen = INT_MAX;  // split mode: lowest level of strip s+1 known to be published
             bool staged_next = false;  // the record of the next level's down child is already in flight
             for (int t = N; t >= t_end; --t) {
@@ -245,6 +258,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) light_kernel(const __grid_co
                 // during level t+1; split mode did so only if strip s+1 had published it
                 // by then, else it waits for it here (the record is needed now)
                 if (SPLIT && !staged_next && t < N && has_right && t + 1 >= j0 + 32) {
+#if AMTC_L2_PROF
+                    const long long w0 = clock64();
+#endif
                     if (seen > t + 1) {
                         int pv = 0;
                         if (lane == 0) {
@@ -262,6 +278,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) light_kernel(const __grid_co
                     }
                     if (lane < (2 + 3 * C) / 2)
                         cp_async16(&S.stg[(t + 1) & 1][2 * lane], &cin[t + 1].d[2 * lane]);
+#if AMTC_L2_PROF
+                    pw += clock64() - w0;
+                    nw += 1;
+#endif
                 }
                 cp_async_wait_all();
                 __syncwarp();
@@ -296,6 +316,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) light_kernel(const __grid_co
                     if (ready) {
                         if (lane < (2 + 3 * C) / 2) cp_async16(&S.stg[t & 1][2 * lane], &cin[t].d[2 * lane]);
                         staged_next = true;
+#if AMTC_L2_PROF
+                        ne += SPLIT ? 1 : 0;
+#endif
                     }
                 }
                 __syncwarp();
@@ -379,6 +402,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) light_kernel(const __grid_co
                 disc *= vld(I.e_r);
             }
             cp_async_wait_all();
+#if AMTC_L2_PROF
+            if (SPLIT && lane == 0) {
+                atomicAdd(&g_lprof[0], (unsigned long long)(clock64() - p0));
+                atomicAdd(&g_lprof[1], (unsigned long long)pw);
+                atomicAdd(&g_lprof[2], (unsigned long long)nw);
+                atomicAdd(&g_lprof[3], (unsigned long long)(N - t_end + 1));
+                atomicAdd(&g_lprof[4], (unsigned long long)ne);
+            }
+#endif
             err = __reduce_or_sync(LFULL, err);
             if (SPLIT && err && s > 0 && lane == 0) {  // never leave strip s-1 waiting
                 __threadfence();
@@ -432,6 +464,14 @@ static int light2_set_smem() {
     return STATUS_OK;
 }
 size_t light2_split_carry_bytes(int N) { return light2_col_bytes<L2_C>(N); }
+int light_profile(unsigned long long out[8], int reset) {
+    if (cudaMemcpyFromSymbol(out, g_lprof, sizeof(unsigned long long) * 8) != cudaSuccess) return STATUS_ECUDA;
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (cudaMemcpyToSymbol(g_lprof, z, sizeof(z)) != cudaSuccess) return STATUS_ECUDA;
+    }
+    return AMTC_L2_PROF ? STATUS_OK : STATUS_EINVAL;
+}
 
 size_t light2_ws_bytes_per_warp(int N) { return light2_carry_bytes<L2_C>(N) + sizeof(Vtx) * 32 * LBG; }
 int light2_warps_per_cta() { return L2_WARPS; }
