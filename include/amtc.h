@@ -306,6 +306,16 @@ int amtc_debug_full_profile(uint64_t out[8], int reset);
    retry passes (4x arenas per retry) and, past the last retry, AMTC_ECAPACITY. */
 void amtc_debug_set_arena_shift(int shift);
 
+/* TESTING HOOK: how amtc_price_crr_tree (and amtc_price_tree_sharded with
+   k = 0 on one rank without a communicator) sweeps one k = 0 tree.  0 (default)
+   automatic: one cooperative wavefront launch (every warp owns a fixed slot of
+   columns and waits on its neighbours' band counters instead of a launch
+   boundary per band), falling back to one launch per band of D levels when the
+   warps cannot be co-resident; 1 always one launch per band; 2..5 the
+   wavefront with (columns per lane M, levels per band D) = (16, 256), (8, 128),
+   (12, 128), (8, 64).  Affects later calls. */
+void amtc_debug_set_tree_shape(int shape);
+
 #ifdef __cplusplus
 }
 #endif

@@ -61,7 +61,7 @@ EXPORTS = ["amtc_price_american_tc", "amtc_price_american_tc_batch", "amtc_price
            "amtc_price_crr_tree", "amtc_comm_unique_id", "amtc_comm_init", "amtc_comm_destroy",
            "amtc_price_tree_sharded", "amtc_debug_set_split_mode", "amtc_debug_set_light_kernel", "amtc_debug_set_full_kernel", "amtc_debug_set_light_split", "amtc_debug_full_profile",
            "amtc_debug_set_arena_shift", "amtc_tree_shard_plan", "amtc_price_american_tc_hedge",
-           "amtc_batch_shard_plan", "amtc_tree_band_plan"]
+           "amtc_batch_shard_plan", "amtc_tree_band_plan", "amtc_debug_set_tree_shape"]
 
 _lib = None
 
@@ -103,6 +103,8 @@ def lib():
                                             C.c_void_p]
         L.amtc_price_american_tc_hedge.argtypes = [C.POINTER(Params), C.c_int32, C.POINTER(Payoff), C.c_double,
                                                    C.POINTER(Quote), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.amtc_debug_set_tree_shape.restype = None
+        L.amtc_debug_set_tree_shape.argtypes = [C.c_int]
         L.amtc_debug_set_arena_shift.restype = None
         L.amtc_debug_set_arena_shift.argtypes = [C.c_int]
         L.amtc_debug_full_profile.argtypes = [C.c_void_p, C.c_int]
@@ -139,6 +141,12 @@ def debug_set_heavy_threshold(tl: int) -> None:
     """Testing hook: route node updates whose children hold > tl vertices to the
     warp-cooperative path (tl <= 0: default)."""
     lib().amtc_debug_set_heavy_threshold(int(tl))
+
+
+def debug_set_tree_shape(shape: int) -> None:
+    """Testing hook: k=0 single-tree sweep -- 0 auto (wavefront), 1 one launch per band,
+    2..5 wavefront shapes (M, D) = (16, 256), (8, 128), (12, 128), (8, 64)."""
+    lib().amtc_debug_set_tree_shape(int(shape))
 
 
 def debug_set_split_mode(mode: int) -> None:
@@ -295,10 +303,10 @@ def price_crr_batch_host(batch, N: int, stream=None) -> np.ndarray:
 # ---------------------------------------------------------------------------
 
 def price_crr_tree(S0: float, K: float, T: float, sigma: float, R: float, N: int, kind: int = PUT,
-                   K2: float = 0.0, stream=None) -> float:
-    """k = 0 CRR price of one (large) tree on the current device."""
+                   K2: float = 0.0, stream=None, flags: int = 0) -> float:
+    """k = 0 CRR price of one (large) tree on the current device (flags: EUROPEAN | CASH)."""
     p = Params(S0, T, sigma, R)
-    y = Payoff(kind, 0, K, K2)
+    y = Payoff(kind, int(flags), K, K2)
     v = C.c_double()
     rc = lib().amtc_price_crr_tree(C.byref(p), N, C.byref(y), C.byref(v), _stream_handle(stream))
     if rc:

@@ -105,8 +105,9 @@ static bool soa_ok(const amtc_batch_soa* b) {
 }
 
 // small device scratch layout (ints)
-enum { SM_HIST = 0, SM_WORK = TC_CLASSES + 1, SM_OVF0, SM_OVF1, SM_WORST, SM_SPLITN, SM_WORK2, SM_VSUM = 32,
-       SM_INTS = 64 };
+enum { SM_HIST = 0, SM_WORK = TC_CLASSES + 1, SM_OVF0, SM_OVF1, SM_WORST, SM_SPLITN, SM_WORK2,
+       SM_VSUM = TC_CLASSES + 8 /* 8-byte aligned */, SM_INTS = TC_CLASSES + 16 };
+static_assert(SM_WORK2 < SM_VSUM && SM_VSUM % 2 == 0 && SM_VSUM + 2 <= SM_INTS, "small scratch layout");
 
 // split mode policy (testing hook amtc_debug_set_split_mode): -1 auto, 0 off, 1 on when it fits
 static int g_split_mode = -1;

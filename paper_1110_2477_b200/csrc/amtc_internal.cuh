@@ -41,7 +41,7 @@ static_assert(sizeof(Quote) == 24, "amtc_quote layout");
 
 void note_launch();
 
-constexpr int TC_CLASSES = 16;
+constexpr int TC_CLASSES = 64;  // cost classes 1 + floor(4 k/h) up to k/h = 15.5 (config 4 reaches 12.5)
 
 // amtc_prepare.cu
 void tc_launch_prepare(const BatchPtrs& in, int64_t n, int N, Quote* out, unsigned char* cls, int* hist,

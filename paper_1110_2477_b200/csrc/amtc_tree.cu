@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <atomic>
 #include <mutex>
 #include <string>
 
@@ -123,6 +124,115 @@ __global__ void __launch_bounds__(TREE_THREADS) tree_band_kernel(TreeConsts c, i
         const int64_t off = (int64_t)lane * TREE_M + q;
         const int64_t j = jw + off;
         if (off < TREE_W && j < jout0 + nout) vout[j - jout0] = V[q];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Wavefront kernel (one GPU): the same bands as tree_band_kernel, but ONE
+// cooperative launch for the whole tree.  Warp w owns output slot w (columns
+// [w W, (w+1) W), W = 32 M - D) at every band; its window at band b is slots w
+// and w+1 of band b-1's output (the dependency cone of D levels).
+// Instead of a launch boundary (and a window copy) per band, warp w waits on
+// two progress counters: slot w+1 has published band b-1 (its producer) and
+// slot w-1 has finished band b-1 (the last reader of the buffer slot w is
+// about to overwrite: two level buffers, ping-pong by band parity).  Bands of
+// different slots overlap in a wavefront; warps right of the level's width
+// exit.  All warps must be co-resident (cooperative launch; the host falls back
+// to one launch per band when they are not).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int TREE_M, int TD, int KIND, bool EURO, bool SCALED>
+__global__ void __launch_bounds__(TREE_THREADS) tree_wave_kernel(TreeConsts c, int N, double* __restrict__ buf0,
+                                                                 double* __restrict__ buf1, int* __restrict__ prog,
+                                                                 int nslots) {
+    constexpr int TW = 32 * TREE_M - TD;  // output columns per slot
+    static_assert(TD <= TW, "the window of a slot spans slots w and w+1 only");
+    static_assert(!SCALED || KIND != KIND_BULL, "the scaled recursion is for puts and calls");
+    const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (w >= nslots) return;  // warp-uniform
+    const int64_t j0 = (int64_t)w * TW;
+    double V[TREE_M], X[TREE_M];
+    int b = 0;
+    for (int t_top = N; t_top > 0; ++b) {
+        const int Dp = min(TD, t_top);
+        const int t_bot = t_top - Dp;
+        if (j0 > t_bot) break;  // the output level has t_bot + 1 columns: this slot is done
+        const double* vin = (b & 1) ? buf1 : buf0;
+        double* vout = (b & 1) ? buf0 : buf1;
+        if (b > 0) {
+            if (lane == 0) {
+                // producer: slot w+1 was active at band b-1 iff its first column <= t_top
+                if (w + 1 < nslots && (int64_t)(w + 1) * TW <= t_top)
+                    while (ld_acquire(prog + w + 1) < b) __nanosleep(16);
+                if (w > 0)
+                    while (ld_acquire(prog + w - 1) < b) __nanosleep(16);
+            }
+            __syncwarp();
+        }
+#pragma unroll
+        for (int q = 0; q < TREE_M; ++q) {
+            const int64_t j = j0 + lane * TREE_M + q;
+            X[q] = exercise_state(c, t_top, j);
+            if (b == 0) V[q] = fmax(exercise_value(c, X[q]), 0.0);  // leaves (t = N)
+            else V[q] = (j <= t_top) ? __ldcg(vin + j) : 0.0;  // beyond the level: ghost columns, never read back
+        }
+        double scale = 1.0;  // SCALED: V = scale * U after the band
+        if (SCALED) {
+            // U_t = V_t / pd^(t_top - t):  U_t(j) = max(E_t(j) / pd^(t_top - t), a U_{t+1}(j) + U_{t+1}(j+1)),
+            // a = pu / pd -- one DFMA per node on the level-to-level chain; the
+            // scaled exercise value follows Es_t = (d / pd) Es_{t+1} + c0 / pd^(t_top - t)
+            const double a = c.pu / c.pd, dr = c.d / c.pd, ipd = 1.0 / c.pd;
+            double g = c.c0;
+            for (int l = 0; l < Dp; ++l) {
+                const double nb = __shfl_down_sync(0xffffffffu, V[0], 1);
+                g *= ipd;
+                scale *= c.pd;
+#pragma unroll
+                for (int q = 0; q < TREE_M; ++q) {
+                    const double vn = (q + 1 < TREE_M) ? V[q + 1] : nb;
+                    X[q] = fma(dr, X[q], g);
+                    const double cont = fma(a, V[q], vn);
+                    V[q] = EURO ? cont : max_nonneg(X[q], cont);
+                }
+            }
+        } else {
+            for (int l = 0; l < Dp; ++l) {
+                const double nb = __shfl_down_sync(0xffffffffu, V[0], 1);
+#pragma unroll
+                for (int q = 0; q < TREE_M; ++q) {
+                    const double vn = (q + 1 < TREE_M) ? V[q + 1] : nb;
+                    double ex;
+                    if (KIND == KIND_BULL) {
+                        X[q] *= c.d;
+                        ex = fmin(fmax(X[q] - c.K, 0.0), c.K2 - c.K);
+                    } else {
+                        X[q] = fma(c.d, X[q], c.c0);
+                        ex = X[q];
+                    }
+                    const double cont = fma(c.pu, V[q], c.pd * vn);
+                    V[q] = EURO ? cont : max_nonneg(ex, cont);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < TREE_M; ++q) {
+            const int off = lane * TREE_M + q;
+            const int64_t j = j0 + off;
+            if (off < TW && j <= t_bot) __stcg(vout + j, SCALED ? V[q] * scale : V[q]);
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release(prog + w, b + 1);
+        t_top = t_bot;
     }
 }
 
@@ -287,6 +397,79 @@ static int64_t tree_cap(int N, int nranks, int D, int64_t mc) {
     return std::max<int64_t>((N + 1 + nranks - 1) / nranks, 2 * mc) + D + 64;
 }
 
+// testing hook amtc_debug_set_tree_shape: 0 auto, 1 one launch per band,
+// 2..5 the wavefront kernel with (M, D) = (16, 256), (8, 128), (12, 128), (8, 64)
+static std::atomic<int> g_tree_shape{0};
+
+template <int M, int TD>
+static cudaError_t wave_launch(const TreeConsts& c, int N, double* b0, double* b1, int* prog, int& nslots,
+                               cudaStream_t s, bool scaled) {
+    constexpr int TW = 32 * M - TD;
+    nslots = (N + 1 + TW - 1) / TW;
+    const unsigned blocks = (unsigned)((nslots * 32 + TREE_THREADS - 1) / TREE_THREADS);
+    void* fn = nullptr;
+#define AMTC_WAVE_FN(K, E) fn = (K != KIND_BULL && scaled) ? (void*)tree_wave_kernel<M, TD, (K == KIND_BULL ? KIND_PUT : K), E, true> \
+                                                           : (void*)tree_wave_kernel<M, TD, K, E, false>
+    if (c.euro) {
+        if (c.kind == KIND_PUT) AMTC_WAVE_FN(KIND_PUT, true);
+        else if (c.kind == KIND_CALL) AMTC_WAVE_FN(KIND_CALL, true);
+        else AMTC_WAVE_FN(KIND_BULL, true);
+    } else {
+        if (c.kind == KIND_PUT) AMTC_WAVE_FN(KIND_PUT, false);
+        else if (c.kind == KIND_CALL) AMTC_WAVE_FN(KIND_CALL, false);
+        else AMTC_WAVE_FN(KIND_BULL, false);
+    }
+#undef AMTC_WAVE_FN
+    cudaError_t e = cudaMemsetAsync(prog, 0, sizeof(int) * (size_t)nslots, s);
+    if (e != cudaSuccess) return e;
+    TreeConsts cc = c;
+    int n = N, ns = nslots;
+    void* args[] = {&cc, &n, &b0, &b1, &prog, &ns};
+    // cooperative: every warp co-resident (the progress waits need it) or an error
+    e = cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(TREE_THREADS), args, 0, s);
+    if (e == cudaSuccess) note_launch();
+    return e;
+}
+
+// one GPU: the whole tree in one wavefront launch; false if it does not fit
+// (too many slots to be co-resident): the caller runs the banded path
+static bool tree_wave(const TreeConsts& c, int N, TreeBufs* B, double* price, cudaStream_t s, int& st) {
+    int shape = g_tree_shape.load();
+    if (shape == 1) return false;
+    if (shape == 0) shape = (N <= 300000) ? 3 : 2;
+    int nslots = 0;
+    double* const b0 = B->p[0];
+    double* const b1 = B->p[1];
+    int* const prog = reinterpret_cast<int*>(B->p[2]);
+    cudaError_t e;
+    int D = 0;
+    const bool scaled = shape >= 10;
+    switch (shape % 10) {
+        case 2: e = wave_launch<16, 256>(c, N, b0, b1, prog, nslots, s, scaled); D = 256; break;
+        case 4: e = wave_launch<12, 128>(c, N, b0, b1, prog, nslots, s, scaled); D = 128; break;
+        case 5: e = wave_launch<8, 64>(c, N, b0, b1, prog, nslots, s, scaled); D = 64; break;
+        case 6: e = wave_launch<4, 64>(c, N, b0, b1, prog, nslots, s, scaled); D = 64; break;
+        case 7: e = wave_launch<6, 96>(c, N, b0, b1, prog, nslots, s, scaled); D = 96; break;
+        case 8: e = wave_launch<4, 32>(c, N, b0, b1, prog, nslots, s, scaled); D = 32; break;
+        default: e = wave_launch<8, 128>(c, N, b0, b1, prog, nslots, s, scaled); D = 128; break;
+    }
+    if (e == cudaErrorCooperativeLaunchTooLarge) {
+        cudaGetLastError();  // clear
+        return false;
+    }
+    if (e != cudaSuccess) { st = cuda_err(e, "tree wave launch"); return true; }
+    // the last band (index nb - 1) writes level 0 into buf1 (nb - 1 even) or buf0
+    const int nb = (N + D - 1) / D;
+    const double* root = ((nb - 1) & 1) ? b0 : b1;
+    e = cudaMemcpyAsync(B->h_pinned, root, sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) { st = cuda_err(e, "tree wave"); return true; }
+    *price = *B->h_pinned;
+    st = STATUS_OK;
+    return true;
+}
+
 // the whole tree, ranks 0..n-1 of comm (comm == nullptr: one GPU, no NCCL)
 static int tree_run(const TreeConsts& c, int N, ncclComm_t comm, int rank, int nranks, double* price,
                     cudaStream_t s) {
@@ -295,6 +478,10 @@ static int tree_run(const TreeConsts& c, int N, ncclComm_t comm, int rank, int n
     const int64_t cap = tree_cap(N, nranks, TREE_D, TREE_MIN_COLS);
     cudaError_t e = B->ensure((size_t)cap);
     if (e != cudaSuccess) return cuda_err(e, "tree buffers");
+    if (!comm && nranks == 1) {
+        int st = STATUS_OK;
+        if (tree_wave(c, N, B, price, s, st)) return st;
+    }
     double* cur = B->p[0];   // own columns of the current level
     double* win = B->p[1];   // input window of the band
     double* nxt = B->p[2];   // own columns of the next level
@@ -395,6 +582,8 @@ int amtc_comm_destroy(void* comm) {
     if (!comm) return STATUS_EINVAL;
     return ncclCommDestroy(static_cast<ncclComm_t>(comm)) == ncclSuccess ? STATUS_OK : STATUS_ENCCL;
 }
+
+void amtc_debug_set_tree_shape(int shape) { g_tree_shape.store(shape); }
 
 int amtc_tree_band_plan(int32_t N, int nranks, int rank, int32_t band, int32_t D, int64_t min_cols,
                         amtc_band* out, int64_t* send, int64_t* recv, int32_t* n_bands) {

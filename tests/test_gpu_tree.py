@@ -39,6 +39,38 @@ def test_crr_tree_matches_oracle(api, N, case):
     assert _close(g, o, N), (N, kind, g, o)
 
 
+# every sweep shape of the single-tree path (testing hook): 1 one launch per
+# band, 2..5 the wavefront kernel with (M, D) = (16, 256), (8, 128), (12, 128),
+# (8, 64): N around the band height D and the slot width 32 M - D
+@pytest.mark.parametrize("shape", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("N", [1, 63, 64, 65, 128, 129, 255, 256, 257, 1000, 4097, 20011])
+def test_crr_tree_shapes_match_oracle(api, shape, N):
+    try:
+        api.debug_set_tree_shape(shape)
+        for case in range(3):
+            kind, K, K2 = CASES[case]
+            g = api.price_crr_tree(100.0, K, 0.8, 0.3, 0.04, N, kind, K2)
+            o = O.price_crr(O.Option(100.0, K, 0.8, 0.3, 0.04, 0.0, kind, K2), N)
+            assert _close(g, o, N), (shape, N, kind, g, o)
+        g = api.price_crr_tree(100.0, 100.0, 0.8, 0.3, 0.04, N, O.PUT, flags=api.EUROPEAN)
+        o = O.price_crr(O.Option(100.0, 100.0, 0.8, 0.3, 0.04, 0.0, O.PUT, american=False), N)
+        assert _close(g, o, N), (shape, N, "european", g, o)
+    finally:
+        api.debug_set_tree_shape(0)
+
+
+def test_crr_tree_wave_repeatable(api):
+    """The wavefront's progress counters are reset per call: repeated calls at
+    different N (slot counts shrinking and growing) give bitwise equal prices."""
+    vals = {}
+    for rep in range(3):
+        for N in (30000, 777, 100000, 5):
+            g = api.price_crr_tree(100.0, 100.0, 1.0, 0.3, 0.05, N, O.PUT)
+            if rep == 0:
+                vals[N] = g
+            assert g == vals[N], (rep, N, g, vals[N])
+
+
 def test_crr_tree_equals_batch_kernel(api):
     b = W.random_small(16, seed=77, k_max=0.0)
     N = 700
