@@ -1088,16 +1088,46 @@ static __device__ __noinline__ int node_update_block(const Fn U, const Fn D, dou
         double x_prev = __shfl_up_sync(FULLM, e.x, 1);
         bool wRp = __shfl_up_sync(FULLM, (int)wr, 1) != 0;
         if (lane == 0) { x_prev = cx; wRp = cwr; }
-        const WV3 w = w_vertices(e, valid, x_prev, wRp, k0 + lane == h.klast, h.wInf_U);
+        // W's vertices of this event (as w_vertices), written straight to Wb: only
+        // the flags and the two crossing positions live across the prefix sum, and
+        // one vertex at a time is built for its store (the WV3 of w_vertices cost
+        // ~40 registers here and spilled around every block)
+        bool h0 = false, h1 = false, h2 = false;
+        double y0 = 0.0, y2 = 0.0;
+        bool wl = false;
+        if (valid && !e.skip) {
+            wl = winL(e);
+            if (wRp != wl) {  // crossing on (x_prev, x)
+                const double e_w = wl ? e.eU : e.eD, e_o = wl ? e.eD : e.eU;
+                const double s_w = wl ? e.sUL : e.sDL, s_o = wl ? e.sDL : e.sUL;
+                if (s_w != s_o) {
+                    y0 = e.x - (e_w - e_o) / (s_w - s_o);
+                    h0 = y0 > x_prev && y0 < e.x;
+                }
+            }
+            h1 = (wl ? e.sUL : e.sDL) != (wr ? e.sUR : e.sDR);
+            if (k0 + lane == h.klast && wr != h.wInf_U) {  // crossing on (x, +inf)
+                const double e_w = wr ? e.eU : e.eD, e_o = wr ? e.eD : e.eU;
+                const double s_w = wr ? e.sUR : e.sDR, s_o = wr ? e.sDR : e.sUR;
+                if (s_o != s_w) {
+                    y2 = e.x + (e_w - e_o) / (s_o - s_w);
+                    h2 = y2 > e.x;
+                }
+            }
+        }
         int tot;
-        const int off = excl_prefix_sum_bits<2>(w.n, lane, tot);  // w.n <= 3
+        const int off = excl_prefix_sum_bits<2>((int)h0 + (int)h1 + (int)h2, lane, tot);  // <= 3
         if (nW + tot > wcap) return DEV_FALLBACK;  // cannot happen
-        // compile-time q: w stays in registers (a runtime index put it in local memory)
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            if (q < w.n) {
-                const WV v = w.get(q);
-                Wb[nW + off + q] = Vtx{v.x, v.f, v.sR};
+        {
+            Vtx* o = Wb + nW + off;
+            if (h0) {
+                const double e_w = wl ? e.eU : e.eD, s_w = wl ? e.sUL : e.sDL;
+                *o++ = Vtx{y0, fma(s_w, y0 - e.x, e_w), s_w};
+            }
+            if (h1) *o++ = Vtx{e.x, fmax(e.eU, e.eD), wr ? e.sUR : e.sDR};
+            if (h2) {
+                const double e_w = wr ? e.eU : e.eD, s_w = wr ? e.sUR : e.sDR, s_o = wr ? e.sDR : e.sUR;
+                *o = Vtx{y2, fma(s_w, y2 - e.x, e_w), s_o};
             }
         }
         nW += tot;
