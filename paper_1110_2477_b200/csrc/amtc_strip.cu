@@ -323,13 +323,28 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
     __syncthreads();
 
     const int item_lo = L.item_lo ? *L.item_lo : 0;
+    const bool split = L.split_S > 0;
+    // Whole-tree mode: each warp's FIRST item is dealt statically, in snake order
+    // over the CTAs (warp w of CTA b takes queue position w G + b, or w G + G-1-b
+    // for odd w); later items come from the atomic ticket counter.  The queue is
+    // ordered heavy-first and the warps of a CTA start together, so with tickets
+    // alone CTA 0 drew the 20 heaviest items of the batch, CTA 1 the next 20, ...
+    // -- one SM then carried several times the mean load, which a batch of about
+    // one item per warp (a multi-GPU slice) never evens out.  Split mode keeps
+    // pure ticket order (strips must be claimed right to left).
+    bool first_item = !split;
     for (;;) {
         int it = 0;
-        if (lane == 0) it = item_lo + atomicAdd(L.work_counter, 1);
-        it = __shfl_sync(FULL, it, 0);
+        if (first_item) {
+            const int G = (int)gridDim.x, b = (int)blockIdx.x;
+            it = item_lo + wib * G + ((wib & 1) ? G - 1 - b : b);
+            first_item = false;
+        } else {
+            if (lane == 0) it = item_lo + (split ? 0 : (int)gridDim.x * WARPS) + atomicAdd(L.work_counter, 1);
+            it = __shfl_sync(FULL, it, 0);
+        }
         if (it >= *L.n_items) break;
         const int code = L.items[it];
-        const bool split = L.split_S > 0;
         const int tree = split ? code / L.split_S : code;  // 2 option + party
         const int s_first = split ? code % L.split_S : N / SW, s_last = split ? s_first : 0;
         const int64_t opt = tree >> 1;
