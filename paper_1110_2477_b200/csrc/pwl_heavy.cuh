@@ -307,7 +307,9 @@ struct Stage {
 // s_cur: z's slope just right of a.  Returns z's slope just left of b.
 // vi0 >= 0: z's state just right of a is already known (vi0, zU0: z_side's
 // outputs at a), otherwise it is evaluated here.
-template <class Out>
+// ENTRY_KNOWN: the caller guarantees vi0 >= 0 or a = -inf, so the entry never
+// evaluates z_side (one inlined copy less in the block update's sweep C).
+template <class Out, bool ENTRY_KNOWN = false>
 __device__ __forceinline__ double emit_open(double a, double b, const Line& LW, const Line& LM, bool hasM,
                                             const Line& LP, bool hasP, const PCtx& c, double s_cur, bool zU0,
                                             Out& st, int vi0 = -1) {
@@ -316,7 +318,7 @@ __device__ __forceinline__ double emit_open(double a, double b, const Line& LW, 
     bool zU;
     double zv;
     if (vi0 >= 0) { vi = vi0; zU = zU0; }
-    else if (isfinite(a)) z_side(LW, LM, hasM, LP, hasP, c, a, true, vi, zU, zv);
+    else if (!ENTRY_KNOWN && isfinite(a)) z_side(LW, LM, hasM, LP, hasP, c, a, true, vi, zU, zv);
     else { vi = hasM ? 1 : 0; zU = zU0; }
     // events closer than xtol() to either end are rounding images of the end
     // vertex itself (e.g. the M line passes through the vertex that defines it)
@@ -331,6 +333,27 @@ __device__ __forceinline__ double emit_open(double a, double b, const Line& LW, 
         // v switches to a line with a smaller slope that comes from above
         // (each crossing is first screened by the sign of the difference at nx,
         // so the division runs only for a crossing that can still win)
+#ifdef AMTC_ROLLED_CROSS
+        // the same four candidates in the same order through ONE inlined copy of
+        // try_cross (code size: sweep C is instruction-fetch bound)
+#pragma unroll 1
+        for (int k = 0; k < 4; ++k) {
+            Line A, Bq;
+            bool on, rising = false;
+            if (k < 3) {
+                A = k == 0 ? LM : (k == 1 ? LP : LW);
+                Bq = V;
+                on = (k == 0 ? (vi != 1 && hasM) : (k == 1 ? (vi != 2 && hasP) : (vi != 0))) && A.s < V.s;
+            } else {
+                if (pos < c.ux && c.ux < nx) nx = c.ux;  // u's kink
+                A = zU ? V : Uq;                         // z's loser overtakes the winner
+                Bq = zU ? Uq : V;
+                rising = c.seller;
+                on = c.seller ? (A.s > Bq.s) : (A.s < Bq.s);
+            }
+            if (on) try_cross(A, Bq, ref, p_in, nx, rising);
+        }
+#else
         if (vi != 1 && hasM && LM.s < V.s) try_cross(LM, V, ref, p_in, nx, false);
         if (vi != 2 && hasP && LP.s < V.s) try_cross(LP, V, ref, p_in, nx, false);
         if (vi != 0 && LW.s < V.s) try_cross(LW, V, ref, p_in, nx, false);
@@ -342,6 +365,7 @@ __device__ __forceinline__ double emit_open(double a, double b, const Line& LW, 
             const Line& Ls = zU ? V : Uq;
             if (c.seller ? (Ls.s > Wn.s) : (Ls.s < Wn.s)) try_cross(Ls, Wn, ref, p_in, nx, c.seller);
         }
+#endif
         if (!(nx < b_in)) break;
         pos = nx;
         const double s_new = z_side(LW, LM, hasM, LP, hasP, c, pos, true, vi, zU, zv);
@@ -399,16 +423,38 @@ __device__ __forceinline__ bool piece_is_w(double x, double f, double s, double 
 #define AMTC_HEAVY_STAT(i)
 #endif
 
+// Code size: the block update is instruction-fetch bound (DESIGN.md section 8:
+// half of the kernel's stall samples are no_inst), so the 5-step warp scans and
+// the window binary searches are rolled loops (config 4: 8.88 -> 7.90 s/step for
+// the scans alone) and sweep C's emit_open calls never inline the entry z_side.
+// -DAMTC_UNROLLED_SCANS / -DAMTC_UNROLLED_RANK / -DAMTC_NO_ENTRY_KNOWN restore
+// the previous forms for A/B builds.
+#ifndef AMTC_UNROLLED_RANK
+#define AMTC_RANK_UNROLL _Pragma("unroll 1")
+#else
+#define AMTC_RANK_UNROLL _Pragma("unroll")
+#endif
+#ifndef AMTC_NO_ENTRY_KNOWN
+#define AMTC_ENTRY_KNOWN_V true
+#else
+#define AMTC_ENTRY_KNOWN_V false
+#endif
+#ifndef AMTC_UNROLLED_SCANS
+#define AMTC_SCAN_UNROLL _Pragma("unroll 1")
+#else
+#define AMTC_SCAN_UNROLL _Pragma("unroll")
+#endif
+
 // warp-level scans
 __device__ __forceinline__ double warp_min(double v) {
-#pragma unroll
+AMTC_SCAN_UNROLL
     for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(FULLM, v, o));
     return v;
 }
 // exclusive suffix min over lanes > lane
 __device__ __forceinline__ double excl_suffix_min(double v, int lane) {
     double x = v;
-#pragma unroll
+AMTC_SCAN_UNROLL
     for (int o = 1; o < 32; o <<= 1) {
         const double y = __shfl_down_sync(FULLM, x, o);
         if (lane + o < 32) x = fmin(x, y);
@@ -419,7 +465,7 @@ __device__ __forceinline__ double excl_suffix_min(double v, int lane) {
 // exclusive prefix min over lanes < lane
 __device__ __forceinline__ double excl_prefix_min(double v, int lane) {
     double x = v;
-#pragma unroll
+AMTC_SCAN_UNROLL
     for (int o = 1; o < 32; o <<= 1) {
         const double y = __shfl_up_sync(FULLM, x, o);
         if (lane >= o) x = fmin(x, y);
@@ -444,7 +490,7 @@ __device__ __forceinline__ int excl_prefix_sum_bits(int v, int lane, int& total)
 }
 __device__ __forceinline__ int excl_prefix_sum(int v, int lane, int& total) {
     int x = v;
-#pragma unroll
+AMTC_SCAN_UNROLL
     for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(FULLM, x, o);
         if (lane >= o) x += y;
@@ -981,14 +1027,14 @@ __device__ __forceinline__ Vtx shfl_vtx(const Vtx& v, int src) {
 
 __device__ __forceinline__ int rank_lt(const Vtx* w, double x) {  // #{m < 32 : w[1+m].x < x}
     int p = 0;
-#pragma unroll
+AMTC_RANK_UNROLL
     for (int s = 16; s > 0; s >>= 1)
         if (w[p + s].x < x) p += s;  // w[p+s] = window element p+s-1
     return p + (w[p + 1].x < x ? 1 : 0);
 }
 __device__ __forceinline__ int rank_le(const Vtx* w, double x) {  // #{m < 32 : w[1+m].x <= x}
     int p = 0;
-#pragma unroll
+AMTC_RANK_UNROLL
     for (int s = 16; s > 0; s >>= 1)
         if (w[p + s].x <= x) p += s;
     return p + (w[p + 1].x <= x ? 1 : 0);
@@ -1223,13 +1269,50 @@ static __device__ __noinline__ int node_update_block(const Fn U, const Fn D, dou
             st.push(wv.x, wv.f, wv.s);
             s_run = wv.s;
         } else if (has) {
+#ifdef AMTC_SWEEPC_MERGED
+            // One inlined copy of emit_open serves both the left tail (ph = 0: only
+            // W's first vertex, once per node) and the vertex's right piece (ph = 1):
+            // two copies made the loop body ~35 KB of code, more than the 32 KB
+            // instruction cache level shared by the SM's warps (half of all stall
+            // samples are instruction-fetch stalls, profiles/r02_ncu_source_calls_N400.txt)
+#pragma unroll 1
+            for (int ph = first_overall ? 0 : 1; ph < 2; ++ph) {
+                Line LWq, LMq, LPq;
+                bool hasMq, hasPq, zUq;
+                double aq, bq, sq;
+                int viq;
+                if (ph == 0) {
+                    const double Mj = fmin(gl, Mnext);
+                    LWq = Line{wv.x, wv.f, sL};
+                    LMq = Line{0.0, Mj, lo};
+                    LPq = Line{0.0, INFINITY, hi};
+                    const double mv = LMq.at(ux);
+                    const double tl = ftol(mv, uf);
+                    zUq = fabs(uf - mv) > tl ? (seller ? uf > mv : uf < mv) : false;
+                    hasMq = true; hasPq = false;
+                    aq = -INFINITY; bq = wv.x; sq = lo; viq = -1;
+                } else {
+                    LWq = Line{wv.x, wv.f, wv.s};
+                    LMq = Line{0.0, Mnext, lo};
+                    LPq = Line{0.0, Pj, hi};
+                    hasMq = isfinite(Mnext); hasPq = true;
+                    double zv;
+                    const double sr_ = z_side(LWq, LMq, hasMq, LPq, true, c, wv.x, true, viq, zUq, zv);
+                    const bool unknown = s_run != s_run;
+                    if (unknown) pending = st.m == 0;
+                    if (unknown || sr_ != s_run) st.push(wv.x, zv, sr_);
+                    aq = wv.x; bq = xn; sq = sr_;
+                }
+                s_run = emit_open<Stage, true>(aq, bq, LWq, LMq, hasMq, LPq, hasPq, c, sq, zUq, st, viq);
+            }
+#else
             const double Mj = fmin(gl, Mnext);
             if (first_overall) {
                 const Line LW{wv.x, wv.f, sL}, LM{0.0, Mj, lo}, LP{0.0, INFINITY, hi};
                 const double mv = LM.at(ux);
                 const double tl = ftol(mv, uf);
                 const bool zU0 = fabs(uf - mv) > tl ? (seller ? uf > mv : uf < mv) : false;
-                s_run = emit_open(-INFINITY, wv.x, LW, LM, true, LP, false, c, lo, zU0, st);
+                s_run = emit_open<Stage, AMTC_ENTRY_KNOWN_V>(-INFINITY, wv.x, LW, LM, true, LP, false, c, lo, zU0, st);
             }
             int vi;
             bool zU;
@@ -1242,7 +1325,8 @@ static __device__ __noinline__ int node_update_block(const Fn U, const Fn D, dou
             } else if (sr_ != s_run) {
                 st.push(wv.x, zv, sr_);
             }
-            s_run = emit_open(wv.x, xn, LWr, LMr, isfinite(Mnext), LPr, true, c, sr_, zU, st, vi);
+            s_run = emit_open<Stage, AMTC_ENTRY_KNOWN_V>(wv.x, xn, LWr, LMr, isfinite(Mnext), LPr, true, c, sr_, zU, st, vi);
+#endif
         }
         const double s_end = s_run;
         // the slope arriving from the left: s_end of the previous lane (all lanes
@@ -1264,7 +1348,7 @@ static __device__ __noinline__ int node_update_block(const Fn U, const Fn D, dou
         }
         int prevl = cnt > 0 ? lane : -1;
         int nextl = cnt > 0 ? lane : 32;
-#pragma unroll
+AMTC_SCAN_UNROLL
         for (int o = 1; o < 32; o <<= 1) {
             const int y = __shfl_up_sync(FULLM, prevl, o);
             if (lane >= o) prevl = max(prevl, y);

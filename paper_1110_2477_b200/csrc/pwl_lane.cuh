@@ -295,11 +295,20 @@ AMTC_HD int lane_pass2(const FnT<SA>& A, double lo, double hi, double ux, double
                 }
             }
         }
+#ifndef AMTC_NO_LANE_MERGED
+        // one inlined copy of push_v for the vertex and the crossing after it (code size:
+        // the solver kernels are instruction-fetch bound)
+#pragma unroll 1
+        for (int rep = 0; rep < (cross ? 2 : 1); ++rep)
+            env.push_v(rep ? yc : x, rep ? fc : Bx, rep ? sp : s_right);
+        if (cross) flat = false;
+#else
         env.push_v(x, Bx, s_right);
         if (cross) {
             env.push_v(yc, fc, sp);
             flat = false;
         }
+#endif
     }
     env.finish();
     env.E.finish();

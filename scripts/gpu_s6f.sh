@@ -13,6 +13,13 @@ p = d["parity"]
 print("$name", [round(x, 1) for x in d["step_ms"]], "ask", p["ask"]["pass"], p["ask"]["fail"], "bid", p["bid"]["pass"], p["bid"]["fail"], flush=True)
 PY
 }
+if [ "$T" = s6g ]; then
+run rolled_lane -DAMTC_ROLLED_SCANS -DAMTC_LANE_MERGED
+run rolled_entry -DAMTC_ROLLED_SCANS -DAMTC_ENTRY_KNOWN
+run rolled_entry_cross -DAMTC_ROLLED_SCANS -DAMTC_ENTRY_KNOWN -DAMTC_ROLLED_CROSS
+run rolled_rank -DAMTC_ROLLED_SCANS -DAMTC_ROLLED_RANK
+exit 0
+fi
 run merged_rolled -DAMTC_SWEEPC_MERGED -DAMTC_ROLLED_SCANS
 run all3 -DAMTC_SWEEPC_MERGED -DAMTC_ROLLED_SCANS -DAMTC_LANE_MERGED
 run rolled -DAMTC_ROLLED_SCANS
