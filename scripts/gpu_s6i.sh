@@ -1,0 +1,12 @@
+#!/bin/bash
+# session 6: validation of the per-shape rolled/unrolled scan loops: full GPU suite, smoke, benches of every config
+mkdir -p gpurun_out
+T=${1:-s6i}
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$T.log 2>&1 || { echo build failed; tail gpurun_out/build_$T.log; exit 1; }
+timeout 1800 python -m pytest tests -m gpu -q -rf --timeout 1500 > gpurun_out/pytest_$T.log 2>&1; echo pytest rc=$?
+grep -E "passed|failed|FAILED|Error" gpurun_out/pytest_$T.log | tail -12
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$T.log 2>&1; echo smoke rc=$?; tail -2 gpurun_out/smoke_$T.log
+for c in 3 1 5 2; do timeout 600 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/bench_c${c}_$T.log 2>&1; echo bench$c rc=$?; done
+timeout 900 python bench.py > gpurun_out/bench_$T.log 2>gpurun_out/bench_$T.err; echo bench rc=$?; tail -c 600 gpurun_out/bench_$T.log
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$T.csv \
+   python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch_$T.log 2>&1; echo ncu-launches rc=$?
