@@ -268,8 +268,11 @@ __device__ __noinline__ bool serve_one(CtaHdr& H, StripSmem<C, B, true>* all, in
     const Fn U = make_fn(M.up, M.un, M.usl, M.ustr), D = make_fn(M.dp, M.dn, M.dsl, M.dstr);
     const bool seller = O.h_seller != 0;
     int nZ = 0;
-    int e = heavy::node_update_block(U, D, M.lo, M.hi, M.ux, M.uf, seller, &all[me].hw, hscr, hcap, zbuf, zcap, nZ,
-                                     lane);
+    // rolled scan loops for the fetch-bound 20-warp batch shape, unrolled ones for the
+    // latency-bound 16-warp split shape (pwl_heavy.cuh, RL)
+    constexpr bool RL = WARPS > 16 && heavy::RL_DEFAULT;
+    int e = heavy::node_update_block<heavy::HWin*, RL>(U, D, M.lo, M.hi, M.ux, M.uf, seller, &all[me].hw, hscr, hcap, zbuf,
+                                                       zcap, nZ, lane);
     if (e == heavy::DEV_FALLBACK) {  // rare shapes: the lane-contiguous update
         if (lane == 0) all[me].zcnt = 0;
         __syncwarp();

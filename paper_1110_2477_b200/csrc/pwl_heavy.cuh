@@ -429,32 +429,34 @@ __device__ __forceinline__ bool piece_is_w(double x, double f, double s, double 
 // the scans alone) and sweep C's emit_open calls never inline the entry z_side.
 // -DAMTC_UNROLLED_SCANS / -DAMTC_UNROLLED_RANK / -DAMTC_NO_ENTRY_KNOWN restore
 // the previous forms for A/B builds.
-#ifndef AMTC_UNROLLED_RANK
-#define AMTC_RANK_UNROLL _Pragma("unroll 1")
-#else
-#define AMTC_RANK_UNROLL _Pragma("unroll")
-#endif
 #ifndef AMTC_NO_ENTRY_KNOWN
 #define AMTC_ENTRY_KNOWN_V true
 #else
 #define AMTC_ENTRY_KNOWN_V false
 #endif
+// RL (rolled loops) is a template parameter of the scans, the rank searches and
+// node_update_block: the 20-warp batch kernel is fetch bound and takes the
+// rolled forms; the 16-warp split-mode kernel runs one strip pipeline per tree,
+// is bound by the latency of a single warp's update and keeps the unrolled
+// forms (config 3: 1.70 s unrolled vs 2.00 s rolled).
 #ifndef AMTC_UNROLLED_SCANS
-#define AMTC_SCAN_UNROLL _Pragma("unroll 1")
+constexpr bool RL_DEFAULT = true;
 #else
-#define AMTC_SCAN_UNROLL _Pragma("unroll")
+constexpr bool RL_DEFAULT = false;
 #endif
 
 // warp-level scans
+template <bool RL = RL_DEFAULT>
 __device__ __forceinline__ double warp_min(double v) {
-AMTC_SCAN_UNROLL
+#pragma unroll(RL ? 1 : 5)
     for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(FULLM, v, o));
     return v;
 }
 // exclusive suffix min over lanes > lane
+template <bool RL = RL_DEFAULT>
 __device__ __forceinline__ double excl_suffix_min(double v, int lane) {
     double x = v;
-AMTC_SCAN_UNROLL
+#pragma unroll(RL ? 1 : 5)
     for (int o = 1; o < 32; o <<= 1) {
         const double y = __shfl_down_sync(FULLM, x, o);
         if (lane + o < 32) x = fmin(x, y);
@@ -463,9 +465,10 @@ AMTC_SCAN_UNROLL
     return lane < 31 ? nx : INFINITY;
 }
 // exclusive prefix min over lanes < lane
+template <bool RL = RL_DEFAULT>
 __device__ __forceinline__ double excl_prefix_min(double v, int lane) {
     double x = v;
-AMTC_SCAN_UNROLL
+#pragma unroll(RL ? 1 : 5)
     for (int o = 1; o < 32; o <<= 1) {
         const double y = __shfl_up_sync(FULLM, x, o);
         if (lane >= o) x = fmin(x, y);
@@ -490,7 +493,7 @@ __device__ __forceinline__ int excl_prefix_sum_bits(int v, int lane, int& total)
 }
 __device__ __forceinline__ int excl_prefix_sum(int v, int lane, int& total) {
     int x = v;
-AMTC_SCAN_UNROLL
+#pragma unroll(RL_DEFAULT ? 1 : 5)
     for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(FULLM, x, o);
         if (lane >= o) x += y;
@@ -1025,16 +1028,18 @@ __device__ __forceinline__ Vtx shfl_vtx(const Vtx& v, int src) {
     return Vtx{__shfl_sync(FULLM, v.x, src), __shfl_sync(FULLM, v.f, src), __shfl_sync(FULLM, v.s, src)};
 }
 
+template <bool RL = RL_DEFAULT>
 __device__ __forceinline__ int rank_lt(const Vtx* w, double x) {  // #{m < 32 : w[1+m].x < x}
     int p = 0;
-AMTC_RANK_UNROLL
+#pragma unroll(RL ? 1 : 5)
     for (int s = 16; s > 0; s >>= 1)
         if (w[p + s].x < x) p += s;  // w[p+s] = window element p+s-1
     return p + (w[p + 1].x < x ? 1 : 0);
 }
+template <bool RL = RL_DEFAULT>
 __device__ __forceinline__ int rank_le(const Vtx* w, double x) {  // #{m < 32 : w[1+m].x <= x}
     int p = 0;
-AMTC_RANK_UNROLL
+#pragma unroll(RL ? 1 : 5)
     for (int s = 16; s > 0; s >>= 1)
         if (w[p + s].x <= x) p += s;
     return p + (w[p + 1].x <= x ? 1 : 0);
@@ -1071,7 +1076,7 @@ __device__ __forceinline__ Ev block_event(const HWin& Wn, int code) {
 }
 
 // z is written to zout[0 .. nZ) (contiguous, capacity zcap)
-template <class WinPtr>
+template <class WinPtr, bool RL = RL_DEFAULT>
 static __device__ __noinline__ int node_update_block(const Fn U, const Fn D, double lo, double hi, double ux, double uf,
                                               bool seller, WinPtr win, Vtx* scratch, int scap, Vtx* zout, int zcap,
                                               int& nZ, int lane) {
@@ -1114,12 +1119,12 @@ static __device__ __noinline__ int node_update_block(const Fn U, const Fn D, dou
         {
             const Vtx uu = Wn.u[1 + lane], dd = Wn.d[1 + lane];
             if (a + lane < U.n) {
-                const int r = rank_lt(Wn.d, uu.x);
+                const int r = rank_lt<RL>(Wn.d, uu.x);
                 const int pos = lane + r;
                 if (pos < nrem) Wn.ev[pos] = 1 | (lane << 1) | (r << 7);
             }
             if (b + lane < D.n) {
-                const int r = rank_le(Wn.u, dd.x);
+                const int r = rank_le<RL>(Wn.u, dd.x);
                 const int pos = lane + r;
                 if (pos < nrem) Wn.ev[pos] = (lane << 1) | (r << 7);
             }
@@ -1215,7 +1220,7 @@ static __device__ __noinline__ int node_update_block(const Fn U, const Fn D, dou
             const Vtx vn = (blk > 0) ? Wb[j - 32] : SENT;  // prefetch the block to the left
             const double g = (j < nW) ? fma(-lo, v.x, v.f) : INFINITY;
             if (lane == 0) Mafter[blk] = Mc;
-            Mc = fmin(Mc, warp_min(g));
+            Mc = fmin(Mc, warp_min<RL>(g));
             v = vn;
             j -= 32;
         }
@@ -1245,8 +1250,8 @@ static __device__ __noinline__ int node_update_block(const Fn U, const Fn D, dou
         if (lane == 31) xn = xn31;
         const double gl = has ? fma(-lo, wv.x, wv.f) : INFINITY;
         const double hl = has ? fma(-hi, wv.x, wv.f) : INFINITY;
-        const double Mnext = fmin(excl_suffix_min(gl, lane), Mafter[blk]);  // g over later W vertices
-        const double hpre = excl_prefix_min(hl, lane);
+        const double Mnext = fmin(excl_suffix_min<RL>(gl, lane), Mafter[blk]);  // g over later W vertices
+        const double hpre = excl_prefix_min<RL>(hl, lane);
         const double Pl = fmin(hpre, Pc);                                   // h over earlier W vertices
         const bool first_overall = has && j == 0;
         Stage st;
@@ -1348,7 +1353,7 @@ static __device__ __noinline__ int node_update_block(const Fn U, const Fn D, dou
         }
         int prevl = cnt > 0 ? lane : -1;
         int nextl = cnt > 0 ? lane : 32;
-AMTC_SCAN_UNROLL
+#pragma unroll(RL ? 1 : 5)
         for (int o = 1; o < 32; o <<= 1) {
             const int y = __shfl_up_sync(FULLM, prevl, o);
             if (lane >= o) prevl = max(prevl, y);
