@@ -420,7 +420,7 @@ def run_amtc(args):
             ach = full_ops / (fm / 1e3) if fm > 0 else 0.0
             roofline = {"bound": "alu", "achieved": ach / 1e12, "peak": instr_peak / 1e12,
                         "unit": "T FP64-instr/s", "frac": ach / instr_peak,
-                        "traffic": None, "kernel": "strip_kernel<4,4,20,1,1> (full; the dominant kernel)",
+                        "traffic": None, "kernel": "strip_kernel<3,3,20,1,1> (full; the dominant kernel)",
                         "kernels": per_k,
                         "work_source": "oracle cost-model ops (SURVEY 8(d): merge 3, crossing 4, restriction 2|4, "
                                        "scaling 2) per option and party, tests/golden/oracle_config4_full.npz",

@@ -640,7 +640,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
 // host side
 // ---------------------------------------------------------------------------
 // full kernel: one CTA of 20 warps per SM (the CTA is the work-sharing domain of
-// tier 3), 4-vertex row slots and scratch (measured: 20 warps / 4 beat 16 / 6 by
+// tier 3), 3-vertex row slots and scratch (20 / 3: 7.48 s vs 20 / 4: 7.65 s per config-4 step with the
+// rolled-scan heavy update; before it measured: 20 warps / 4 beat 16 / 6 by
 // 2.5%, 12 / 6 and 8 / 6 lose 5-16%, 24 / 3 loses 2.5x).  Light kernel: no tier 3, three CTAs of 8 warps per SM (24 warps,
 // <= 85 registers), for the items that never grow heavy nodes (every seller,
 // every put buyer: DESIGN.md section 5); a heavy node there aborts the item,
@@ -649,7 +650,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) strip_kernel(const __grid_co
 #define AMTC_FULL_WARPS 20
 #endif
 #ifndef AMTC_FULL_CB
-#define AMTC_FULL_CB 4
+#define AMTC_FULL_CB 3
 #endif
 constexpr int STRIP_C = AMTC_FULL_CB, STRIP_B = AMTC_FULL_CB, STRIP_WARPS = AMTC_FULL_WARPS, STRIP_MINB = 1;
 #ifndef AMTC_LIGHT_CFG
